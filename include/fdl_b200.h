@@ -1,0 +1,193 @@
+/*
+ * fdl_b200.h — C ABI of the B200-native Fourier Disparity Layer hot paths.
+ *
+ * The reference (`fdl`, /root/reference/pkg/src/fdl) is pure Python/numpy and
+ * has no FFI of its own; these entry points are what its Python layer would
+ * bind (ctypes stub in INTEGRATION.md) to replace, stage by stage:
+ *
+ *   fdl_views_to_spectra   np.pad + np.fft.rfft2 + sum |b|^2   construct.py:250-266
+ *   fdl_solve_bins         _phase_tables/_system_chunk/_solve_chunk
+ *                          (per-frequency regularised LS)      construct.py:68-80,168-211,277-284
+ *   fdl_symmetrize         self-conjugate column post-pass      construct.py:286-297
+ *   fdl_render_spectra     evaluate_scaled_grid + _weighted_layer_sum
+ *                                                               lfmodel.py:101-122, render.py:190-207,238-245
+ *   fdl_spectra_to_images  irfft_fast + crop + srgb_encode      spectra.py:202-208, render.py:210-225
+ *
+ * Conventions (all calls):
+ *   - return 0 (FDL_OK) on success, a negative FDL_ERR_* code otherwise; the
+ *     message is available from fdl_last_error() (thread-local);
+ *   - every buffer named *_dev is caller-allocated DEVICE memory, every other
+ *     pointer is HOST memory read during the call (not retained);
+ *   - work is enqueued on `stream` (a cudaStream_t, NULL = legacy default
+ *     stream) and is stream-ordered; no call synchronises the device unless
+ *     stated; no global mutable state is shared between calls (re-entrant,
+ *     one call per stream at a time);
+ *   - complex numbers are interleaved (re, im) pairs: fdl_c64 = 2 x float.
+ *
+ * Data layouts in HBM:
+ *   views    (m, H, W, C)            float32   (ViewSet.images order, lfmodel.py:125-191)
+ *   spectra  (m, C, rows, Whp)       fdl_c64   Whp = Wp/2 + 1 (half-plane, spectra.py:41-101)
+ *   layers   (n, C, rows, Whp)       fdl_c64   (FDL1 file order, io.py:175)
+ *   images   (V, H, W, C)            float32
+ * where `rows` is the number of frequency rows of the slab held by this call
+ * (all Hp rows on one GPU; a mirrored-pair slab on a multi-GPU shard).
+ */
+#ifndef FDL_B200_H
+#define FDL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDL_OK 0
+#define FDL_ERR_INVALID -1      /* invalid argument (reference: ValueError) */
+#define FDL_ERR_CUDA -2         /* CUDA / cuFFT failure */
+#define FDL_ERR_UNSUPPORTED -3  /* shape outside this build's kernels */
+#define FDL_ERR_RANK -4         /* singular unregularised system (reference: RankDeficiencyError) */
+
+/* per-bin status written by fdl_solve_bins */
+#define FDL_BIN_OK 0
+#define FDL_BIN_BREAKDOWN 1     /* Cholesky pivot <= 0 or non-finite result */
+
+typedef struct fdl_c64 { float re, im; } fdl_c64;
+
+/* Sampled aperture spectrum psi_hat (ApertureSpec, lfmodel.py:39-122).
+ * table is (rows, cols) row-major, float64; table_im NULL for a real table.
+ * Axis k has node i at xi0_k + i * step_k (lfmodel.py:72-79 uses
+ * step = xi[1] - xi[0] and pos = (q - xi[0]) / step). */
+typedef struct fdl_aperture {
+  int32_t rows, cols;
+  const double* table_re;
+  const double* table_im;
+  double xi0_x, step_x;
+  double xi0_y, step_y;
+} fdl_aperture;
+
+/* ------------------------------------------------------------------------ */
+/* Library                                                                   */
+/* ------------------------------------------------------------------------ */
+
+int fdl_version(void);
+const char* fdl_last_error(void);
+
+/* Device self-test of the FP64 tensor-core (DMMA) fragment layouts the K1
+ * kernels rely on; *max_err receives the largest deviation (synchronises). */
+int fdl_selftest(double* max_err);
+
+/* ------------------------------------------------------------------------ */
+/* K0: pad + R2C + per-view sum |b|^2   (construct.py:250-266)               */
+/* ------------------------------------------------------------------------ */
+
+/* Bytes of device workspace fdl_views_to_spectra needs. */
+size_t fdl_views_to_spectra_workspace(int32_t m, int32_t H, int32_t W, int32_t C, int32_t pad);
+
+/* views_dev (m,H,W,C) f32 -> spectra_dev (m,C,Hp,Whp) c64 with Hp = H + 2 pad,
+ * Wp = W + 2 pad; view_sumsq_dev (m) float64 receives sum_{c,q} |b|^2 per view
+ * (the joint-over-channels numerator of default_lambda, construct.py:214-216). */
+int fdl_views_to_spectra(const float* views_dev, int32_t m, int32_t H, int32_t W, int32_t C,
+                         int32_t pad, fdl_c64* spectra_dev, double* view_sumsq_dev,
+                         void* workspace_dev, size_t workspace_bytes, void* stream);
+
+/* Gather whole frequency rows of view spectra into a contiguous slab:
+ * dst (m, C, nrows, Whp) <- src (m, C, Hp, Whp)[..., rows[i], :].  Used to pack
+ * the all-to-all send buffers of the multi-GPU path. */
+int fdl_gather_rows(const fdl_c64* src_dev, int32_t m, int32_t C, int32_t Hp, int32_t Whp,
+                    const int32_t* rows_dev, int32_t nrows, fdl_c64* dst_dev, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* K1: per-bin regularised least squares   (construct.py:168-211)           */
+/* ------------------------------------------------------------------------ */
+
+typedef struct fdl_solve_desc {
+  int32_t m, n, C;         /* views, layers, channels */
+  int32_t Hp, Wp;          /* padded grid; Whp = Wp/2 + 1 */
+  int32_t nrows;           /* frequency rows in this slab */
+  const int32_t* rows;     /* host, nrows ky indices (NULL: rows 0..nrows-1) */
+  /* shift model (ShiftParams, lfmodel.py:204-267): factored (u, v) or relaxed (pu, pv) */
+  const double* u;         /* host, m (NULL when relaxed) */
+  const double* v;         /* host, m */
+  const double* pu;        /* host, m*n row-major (NULL when factored) */
+  const double* pv;        /* host, m*n */
+  const double* d;         /* host, n layer disparities */
+  /* wide-aperture views (construct.py:170-179); view_aperture NULL = all pinhole */
+  const int32_t* view_aperture; /* host, m: index into apertures or -1 for a pinhole */
+  const double* s;         /* host, m refocus parameters */
+  const double* scale;     /* host, m aperture scales */
+  int32_t n_apertures;
+  const fdl_aperture* apertures;
+  double lam, eps;         /* lambda (>= 0) and the absolute eps of reg (construct.py:283) */
+  const fdl_c64* spectra_dev;  /* (m, C, nrows, Whp) */
+  fdl_c64* layers_dev;         /* (n, C, nrows, Whp) */
+  int8_t* status_dev;          /* (nrows, Whp) FDL_BIN_* or NULL */
+  int32_t force_path;          /* 0 = auto; 1 = symmetric-real, 2 = real-A, 3 = complex embedding;
+                                  4 = auto formulation on the generic (non-DMMA) kernel (testing) */
+} fdl_solve_desc;
+
+/* Bytes of device workspace fdl_solve_bins needs (0 for the current kernels
+ * beyond the parameter block; always query). */
+size_t fdl_solve_bins_workspace(const fdl_solve_desc* desc);
+
+/* Solve every bin of the slab.  Returns FDL_OK even when some bins break
+ * down; they are flagged in status_dev (and counted in *n_breakdown when
+ * non-NULL, which synchronises the stream). */
+int fdl_solve_bins(const fdl_solve_desc* desc, void* workspace_dev, size_t workspace_bytes,
+                   int32_t* n_breakdown, void* stream);
+
+/* Which path fdl_solve_bins picks for this descriptor (1, 2, 3 as force_path). */
+int fdl_solve_path(const fdl_solve_desc* desc);
+
+/* ------------------------------------------------------------------------ */
+/* K2: conjugate-pair symmetrisation of self-conjugate columns (construct.py:286-297) */
+/* ------------------------------------------------------------------------ */
+
+/* layers (n, C, nrows, Whp); rows/mirror are host arrays: mirror[i] is the
+ * slab index of row (Hp - rows[i]) % Hp (must be in the slab). */
+int fdl_symmetrize(fdl_c64* layers_dev, int32_t n, int32_t C, int32_t Hp, int32_t Wp,
+                   int32_t nrows, const int32_t* rows, const int32_t* mirror, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* K3: batched render spectra   (render.py:190-207, lfmodel.py:101-122)      */
+/* ------------------------------------------------------------------------ */
+
+typedef struct fdl_render_desc {
+  int32_t n, C, Hp, Wp;    /* layers (n, C, Hp, Whp) */
+  int32_t V;               /* output views in this batch */
+  const double* d;         /* host, n */
+  const double* pu;        /* host, V*n per-(view, layer) x shifts (u_v * d_k for render) */
+  const double* pv;        /* host, V*n */
+  const double* t;         /* host, V*n aperture scale t = f (s - d_k); ignored where view_aperture < 0 */
+  const int32_t* view_aperture; /* host, V (NULL = all pinhole) */
+  int32_t n_apertures;
+  const fdl_aperture* apertures;
+  const fdl_c64* layers_dev;
+  fdl_c64* out_dev;        /* (V, C, Hp, Whp) */
+  int64_t* oob_dev;        /* (V) out-of-range aperture lookups (lfmodel.py:118-121), or NULL */
+} fdl_render_desc;
+
+size_t fdl_render_workspace(const fdl_render_desc* desc);
+int fdl_render_spectra(const fdl_render_desc* desc, void* workspace_dev, size_t workspace_bytes,
+                       void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* K4: C2R + crop + optional sRGB   (spectra.py:202-208, render.py:210-225) */
+/* ------------------------------------------------------------------------ */
+
+size_t fdl_spectra_to_images_workspace(int32_t V, int32_t C, int32_t Hp, int32_t Wp);
+
+/* spectra (V, C, Hp, Whp) c64 (DESTROYED: used as the C2R input; its
+ * self-conjugate columns are first projected onto their Hermitian part, which
+ * is what numpy's irfft2 inverts) -> images (V, Ho, Wo, C) f32, cropped to [pad, pad+Ho) x
+ * [pad, pad+Wo) (pass pad = 0, Ho = Hp, Wo = Wp for no crop), sRGB-encoded
+ * when srgb != 0. */
+int fdl_spectra_to_images(fdl_c64* spectra_dev, int32_t V, int32_t C, int32_t Hp,
+                          int32_t Wp, int32_t pad, int32_t Ho, int32_t Wo, int32_t srgb,
+                          float* images_dev, void* workspace_dev, size_t workspace_bytes,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDL_B200_H */

@@ -1,0 +1,62 @@
+"""B200-native Fourier Disparity Layers: the construction and rendering hot paths.
+
+Drop-in for the reference package `fdl` on these paths (same names, argument
+meaning and exceptions as fdl/__init__.py:3-98 for everything below); the
+compute runs in hand-written sm_100a CUDA kernels behind a C ABI
+(include/fdl_b200.h, libfdl_b200.so).  Out of scope:
+calibration, pipelines, I/O, CLI, HTTP service, viewer.
+"""
+
+from .spectra import DFT_CONVENTION, FrequencyGrid
+from .lfmodel import GAMMA, LINEAR, ApertureSpec, FdlModel, ShiftParams, ViewSet, expand_shifts
+from .construct import (
+    DEFAULT_EPS,
+    SOLVE_CHUNK,
+    RankDeficiencyError,
+    construct_fdl,
+    default_lambda,
+    last_construct_stats,
+    view_regularizer,
+)
+from .render import (
+    RenderRequest,
+    RenderStats,
+    aperture_spectrum,
+    last_render_stats,
+    render,
+    render_many,
+    render_views_with_shifts,
+    srgb_decode,
+    srgb_encode,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DFT_CONVENTION",
+    "FrequencyGrid",
+    "GAMMA",
+    "LINEAR",
+    "ApertureSpec",
+    "FdlModel",
+    "ShiftParams",
+    "ViewSet",
+    "expand_shifts",
+    "DEFAULT_EPS",
+    "SOLVE_CHUNK",
+    "RankDeficiencyError",
+    "construct_fdl",
+    "default_lambda",
+    "last_construct_stats",
+    "view_regularizer",
+    "RenderRequest",
+    "RenderStats",
+    "aperture_spectrum",
+    "last_render_stats",
+    "render",
+    "render_many",
+    "render_views_with_shifts",
+    "srgb_decode",
+    "srgb_encode",
+    "__version__",
+]

@@ -1,0 +1,266 @@
+"""FDL construction on the B200 (reference: fdl/construct.py:219-308).
+
+`construct_fdl` keeps the reference signature, defaults and exceptions; the
+work runs as three native stages through the C ABI (include/fdl_b200.h):
+
+  K0 fdl_views_to_spectra  pad + cuFFT R2C + per-view sum |b|^2  (construct.py:250-266)
+  K1 fdl_solve_bins        per-bin fp64 regularised LS            (construct.py:68-80,168-211)
+  K2 fdl_symmetrize        self-conjugate column post-pass        (construct.py:286-297)
+
+The default lambda (construct.py:214-216) is 1e-4 * sum|b|^2 / (Q m), with the
+per-view partial sums added in view order so the value does not depend on how
+the views are sharded across GPUs.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _native as nat
+from .lfmodel import FdlModel, ShiftParams, ViewSet, _is_torch
+from .spectra import FrequencyGrid
+
+__all__ = [
+    "RankDeficiencyError",
+    "DEFAULT_EPS",
+    "SOLVE_CHUNK",
+    "view_regularizer",
+    "default_lambda",
+    "construct_fdl",
+    "ConstructStats",
+    "last_construct_stats",
+]
+
+DEFAULT_EPS = 1e-9       # construct.py:27
+SOLVE_CHUNK = 16384      # construct.py:28 (accepted for API compatibility; K1 has no chunking)
+
+
+class RankDeficiencyError(Exception):
+    """Unregularized normal matrix is singular at some frequency (construct.py:32-33)."""
+
+
+def view_regularizer(omega_x, omega_y, d, eps: float = DEFAULT_EPS):
+    """Diagonal (wx^2+wy^2)^2 d_k^4 + eps of the view regulariser (construct.py:36-45)."""
+    w4 = (np.asarray(omega_x, float) ** 2 + np.asarray(omega_y, float) ** 2) ** 2
+    return w4[..., None] * np.asarray(d, float) ** 4 + eps
+
+
+def default_lambda(b_norms_sq, m: int) -> float:
+    """1e-4 * mean_q ||b_q||^2 / m (construct.py:214-216)."""
+    return 1e-4 * float(np.mean(b_norms_sq)) / m
+
+
+class ConstructStats:
+    """Breakdown of the last construct_fdl call on this thread (host seconds)."""
+
+    def __init__(self):
+        self.path = 0
+        self.breakdown_bins = 0
+        self.lam = None
+
+
+import threading
+
+_tls = threading.local()
+
+
+def last_construct_stats() -> ConstructStats:
+    st = getattr(_tls, "stats", None)
+    if st is None:
+        st = _tls.stats = ConstructStats()
+    return st
+
+
+def _require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1901_06919_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def _views_device(images, device):
+    """(m,H,W,C) float32 contiguous CUDA tensor."""
+    import torch
+    if _is_torch(images):
+        t = images
+    else:
+        arr = np.ascontiguousarray(images, dtype=np.float32)
+        t = torch.from_numpy(arr)
+        if device.type == "cuda":
+            t = t.pin_memory() if arr.nbytes >= (1 << 20) else t
+    return t.to(device=device, dtype=torch.float32, non_blocking=True).contiguous()
+
+
+def aperture_table_set(apertures):
+    """Unique non-pinhole ApertureSpecs and per-view indices (-1 for pinholes)."""
+    uniq, idx = [], []
+    for ap in apertures:
+        if ap is None or ap.is_pinhole:
+            idx.append(-1)
+            continue
+        for i, u in enumerate(uniq):
+            if u is ap:
+                idx.append(i)
+                break
+        else:
+            uniq.append(ap)
+            idx.append(len(uniq) - 1)
+    return uniq, np.asarray(idx, dtype=np.int32)
+
+
+def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps, views=None,
+               u=None, v=None, force_path=0, status=None):
+    """Run K1 on a slab of frequency rows; returns (layers (n,C,nrows,Whp) c64, n_breakdown, path)."""
+    import torch
+    device = spectra.device
+    whp = Wp // 2 + 1
+    nrows = len(rows)
+    layers = torch.empty((n, C, nrows, whp), dtype=torch.complex64, device=device)
+    if status is None:
+        status = torch.zeros((nrows, whp), dtype=torch.int8, device=device)
+    rows_np = np.ascontiguousarray(rows, dtype=np.int32)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    keep = [rows_np, d]
+    desc = nat.FdlSolveDesc()
+    desc.m, desc.n, desc.C, desc.Hp, desc.Wp, desc.nrows = m, n, C, Hp, Wp, nrows
+    desc.rows = nat.iptr(rows_np)
+    if u is not None:
+        u_ = np.ascontiguousarray(u, dtype=np.float64)
+        v_ = np.ascontiguousarray(v, dtype=np.float64)
+        keep += [u_, v_]
+        desc.u, desc.v = nat.dptr(u_), nat.dptr(v_)
+    else:
+        pu_ = np.ascontiguousarray(shifts_pu, dtype=np.float64)
+        pv_ = np.ascontiguousarray(shifts_pv, dtype=np.float64)
+        keep += [pu_, pv_]
+        desc.pu, desc.pv = nat.dptr(pu_), nat.dptr(pv_)
+    desc.d = nat.dptr(d)
+    if views is not None and not views.all_pinhole:
+        uniq, idx = aperture_table_set(views.apertures)
+        arr, keep_ap = nat.aperture_structs(uniq)
+        s_ = np.ascontiguousarray(views.s, dtype=np.float64)
+        sc_ = np.ascontiguousarray(views.aperture_scale, dtype=np.float64)
+        keep += [idx, s_, sc_, arr, keep_ap]
+        desc.view_aperture = nat.iptr(idx)
+        desc.s, desc.scale = nat.dptr(s_), nat.dptr(sc_)
+        desc.n_apertures = len(uniq)
+        desc.apertures = arr
+    desc.lam, desc.eps = float(lam), float(eps)
+    desc.spectra_dev = spectra.data_ptr()
+    desc.layers_dev = layers.data_ptr()
+    desc.status_dev = status.data_ptr()
+    desc.force_path = int(force_path)
+    L = nat.lib()
+    path = L.fdl_solve_path(desc)
+    if path < 0:
+        nat.check(path, "fdl_solve_path")
+    ws_bytes = L.fdl_solve_bins_workspace(desc)
+    if ws_bytes == 0:
+        nat.check(L.fdl_solve_path(desc), "fdl_solve_bins_workspace")
+    ws = nat.workspace(ws_bytes, device)
+    nb = nat.ctypes.c_int32(0)
+    nat.check(L.fdl_solve_bins(desc, ws.data_ptr(), ws.numel(), nat.ctypes.byref(nb),
+                               nat.stream_handle(device)), "fdl_solve_bins")
+    return layers, int(nb.value), path
+
+
+def views_to_spectra(views_dev, pad):
+    """K0 on a (m,H,W,C) float32 CUDA tensor -> (spectra (m,C,Hp,Whp) c64, per-view sum|b|^2 (m) f64)."""
+    import torch
+    m, H, W, C = views_dev.shape
+    Hp, Wp = H + 2 * pad, W + 2 * pad
+    device = views_dev.device
+    spectra = torch.empty((m, C, Hp, Wp // 2 + 1), dtype=torch.complex64, device=device)
+    sumsq = torch.empty((m,), dtype=torch.float64, device=device)
+    L = nat.lib()
+    ws_bytes = L.fdl_views_to_spectra_workspace(m, H, W, C, pad)
+    if ws_bytes == 0:
+        raise nat.FdlNativeError("fdl_views_to_spectra_workspace: " + L.fdl_last_error().decode())
+    ws = nat.workspace(ws_bytes, device)
+    nat.check(L.fdl_views_to_spectra(views_dev.data_ptr(), m, H, W, C, pad, spectra.data_ptr(),
+                                     sumsq.data_ptr(), ws.data_ptr(), ws.numel(),
+                                     nat.stream_handle(device)), "fdl_views_to_spectra")
+    return spectra, sumsq
+
+
+def symmetrize(layers, Hp, Wp, rows=None, mirror=None):
+    n, C, nrows, _ = layers.shape
+    L = nat.lib()
+    r = np.ascontiguousarray(rows, dtype=np.int32) if rows is not None else None
+    mi = np.ascontiguousarray(mirror, dtype=np.int32) if mirror is not None else None
+    nat.check(L.fdl_symmetrize(layers.data_ptr(), n, C, Hp, Wp, nrows, nat.iptr(r), nat.iptr(mi),
+                               nat.stream_handle(layers.device)), "fdl_symmetrize")
+
+
+def resolve_shifts(views: ViewSet, shifts: ShiftParams):
+    """Validation of construct.py:234-248; returns (pu, pv, d)."""
+    pu, pv = shifts.expand()
+    m = views.num_views
+    if pu.shape[0] != m:
+        raise ValueError(f"shift parameters describe {pu.shape[0]} views, got {m}")
+    if shifts.d is None:
+        raise ValueError("relaxed shift parameters need layer disparities attached")
+    d = np.asarray(shifts.d, dtype=np.float64)
+    return pu, pv, d
+
+
+def default_pad_margin(pu, pv) -> int:
+    """ceil(max |P|) (construct.py:250-252)."""
+    if pu.size == 0:
+        return 0
+    return int(math.ceil(max(np.max(np.abs(pu)), np.max(np.abs(pv)))))
+
+
+def lambda_from_sumsq(view_sumsq, Q: int, m: int) -> float:
+    """default_lambda from per-view partial sums, summed on the host in view order."""
+    tot = 0.0
+    for s in np.asarray(view_sumsq, dtype=np.float64):
+        tot += float(s)
+    return 1e-4 * (tot / Q) / m
+
+
+def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None, eps: float = DEFAULT_EPS,
+                  pad_margin: int | None = None, chunk: int = SOLVE_CHUNK, *, device=None,
+                  force_path: int = 0) -> FdlModel:
+    """Build the disparity-layer model by per-frequency solves (construct.py:219-308).
+
+    Same arguments, defaults and exceptions as the reference.  `chunk` is
+    accepted and ignored (every bin is solved independently in one launch;
+    results never depend on it).  `device` picks the CUDA device (default:
+    current); `force_path` pins the K1 formulation (testing).
+    """
+    torch = _require_cuda()
+    pu, pv, d = resolve_shifts(views, shifts)
+    m = views.num_views
+    n = pu.shape[1]
+    if lam == 0 and n > m:
+        raise RankDeficiencyError(f"{n} layers from {m} images is ill-posed without regularization")
+    if pad_margin is None:
+        pad_margin = default_pad_margin(pu, pv)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    H, W, C = views.height, views.width, views.channels
+    Hp, Wp = H + 2 * pad_margin, W + 2 * pad_margin
+    grid = FrequencyGrid(width=Wp, height=Hp)
+    views_dev = _views_device(views.images, dev)
+    spectra, sumsq = views_to_spectra(views_dev, pad_margin)
+    del views_dev
+    if lam is None:
+        lam = lambda_from_sumsq(sumsq.cpu().numpy(), grid.num_entries, m)
+    if lam < 0:
+        raise ValueError("lam must be non-negative")
+    u = views_u = None
+    if shifts.is_factored:
+        u, views_u = shifts.u, shifts.v
+    layers, n_bad, path = solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, lam, eps,
+                                     views=views, u=u, v=views_u, force_path=force_path)
+    st = last_construct_stats()
+    st.path, st.breakdown_bins, st.lam = path, n_bad, float(lam)
+    if n_bad:
+        if lam == 0:
+            raise RankDeficiencyError("singular normal matrix at some frequency")
+        raise nat.FdlNativeError(f"{n_bad} bins broke down in the fp64 Cholesky (min-norm fallback pending)")
+    symmetrize(layers, Hp, Wp)
+    return FdlModel(disparities=d, layers=layers, grid=grid, width=W, height=H, pad_margin=pad_margin,
+                    color_space=views.color_space, calibration=shifts, lambda_used=float(lam))

@@ -1,0 +1,632 @@
+// C ABI of libfdl_b200 (include/fdl_b200.h): argument validation, parameter
+// staging and kernel dispatch.  No global mutable state besides per-thread
+// caches (error string, pinned staging ring, cuFFT plans).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "k1_solve.cuh"
+#include "k3_render.cuh"
+
+namespace fdl {
+
+// --- k0_spectra.cu / k1_*.cu -------------------------------------------------
+int views_to_spectra_ws(int m, int H, int W, int C, int pad, size_t* bytes);
+int views_to_spectra(const float* views, int m, int H, int W, int C, int pad, fdl_c64* spectra, double* view_sumsq,
+                     void* ws, size_t ws_bytes, cudaStream_t st);
+int gather_rows(const fdl_c64* src, int m, int C, int Hp, int Whp, const int* rows_dev, int nrows, fdl_c64* dst,
+                cudaStream_t st);
+int spectra_to_images_ws(int V, int C, int Hp, int Wp, size_t* bytes);
+int spectra_to_images(fdl_c64* spectra, int V, int C, int Hp, int Wp, int pad, int Ho, int Wo, int srgb,
+                      float* images, void* ws, size_t ws_bytes, cudaStream_t st);
+int k1_generic_launch(const SolveParams& p, cudaStream_t st);
+int k1_fast_launch(const SolveParams& p, cudaStream_t st, bool* handled);
+int selftest_dmma(cudaStream_t st, double* max_err);
+
+// --- errors --------------------------------------------------------------------
+thread_local std::string t_error;
+void set_error(const std::string& msg) { t_error = msg; }
+int fail(int code, const std::string& msg) {
+  t_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  t_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return FDL_ERR_CUDA;
+}
+
+namespace {
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Host-side image of a parameter block; offsets are relative to the device base.
+struct Blob {
+  std::vector<char> bytes;
+  size_t add(const void* src, size_t n) {
+    size_t off = align256(bytes.size());
+    bytes.resize(off + n);
+    if (n) std::memcpy(bytes.data() + off, src, n);
+    return off;
+  }
+  size_t reserve(size_t n) {
+    size_t off = align256(bytes.size());
+    bytes.resize(off + n);
+    return off;
+  }
+  size_t size() const { return align256(bytes.size()); }
+};
+
+// Pinned staging ring: the H2D copy of a parameter block must not read
+// pageable memory (that would synchronise the stream).
+struct StageSlot {
+  char* ptr = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+};
+thread_local StageSlot t_stage[4];
+thread_local int t_stage_next = 0;
+
+int upload(const Blob& b, void* dev, cudaStream_t st) {
+  if (b.bytes.empty()) return FDL_OK;
+  StageSlot& s = t_stage[t_stage_next];
+  t_stage_next = (t_stage_next + 1) & 3;
+  if (s.pending) FDL_CUDA_CHECK(cudaEventSynchronize(s.ev));
+  if (s.cap < b.bytes.size()) {
+    if (s.ptr) cudaFreeHost(s.ptr);
+    s.cap = std::max(b.bytes.size(), (size_t)1 << 16) * 2;
+    FDL_CUDA_CHECK(cudaMallocHost(&s.ptr, s.cap));
+  }
+  if (!s.ev) FDL_CUDA_CHECK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+  std::memcpy(s.ptr, b.bytes.data(), b.bytes.size());
+  FDL_CUDA_CHECK(cudaMemcpyAsync(dev, s.ptr, b.bytes.size(), cudaMemcpyHostToDevice, st));
+  FDL_CUDA_CHECK(cudaEventRecord(s.ev, st));
+  s.pending = true;
+  return FDL_OK;
+}
+
+template <class T>
+const T* at(void* base, size_t off) {
+  return reinterpret_cast<const T*>(reinterpret_cast<char*>(base) + off);
+}
+
+// ---------------------------------------------------------------------------
+// K1 planning
+// ---------------------------------------------------------------------------
+struct SolvePlan {
+  Blob blob;
+  SolveParams p{};
+  size_t o_rows, o_pu, o_pv, o_d, o_d4, o_vap, o_s, o_sc, o_aps, o_cnt;
+  size_t o_uidx = 0, o_vidx = 0, o_uval = 0, o_vval = 0;
+  bool has_axes = false;
+  std::vector<size_t> o_tab_re, o_tab_im;
+};
+
+bool finite_all(const double* x, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(x[i])) return false;
+  return true;
+}
+
+int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
+  if (!D) return fail(FDL_ERR_INVALID, "null descriptor");
+  const int m = D->m, n = D->n, C = D->C;
+  if (m < 1 || n < 1 || C < 1) return fail(FDL_ERR_INVALID, "m, n and C must be positive");
+  if (D->Hp < 1 || D->Wp < 1) return fail(FDL_ERR_INVALID, "invalid grid dimensions");
+  if (D->nrows < 0 || D->nrows > D->Hp) return fail(FDL_ERR_INVALID, "invalid slab row count");
+  if (!D->d) return fail(FDL_ERR_INVALID, "layer disparities required");
+  if (!(D->lam >= 0.0) || !std::isfinite(D->lam)) return fail(FDL_ERR_INVALID, "lam must be non-negative");
+  const bool factored = D->u && D->v;
+  if (!factored && !(D->pu && D->pv)) return fail(FDL_ERR_INVALID, "need (u, v) or (pu, pv)");
+  if (!finite_all(D->d, n)) return fail(FDL_ERR_INVALID, "disparities must be finite");
+  std::vector<int> rows(D->nrows);
+  for (int i = 0; i < D->nrows; ++i) {
+    rows[i] = D->rows ? D->rows[i] : i;
+    if (rows[i] < 0 || rows[i] >= D->Hp) return fail(FDL_ERR_INVALID, "slab row out of range");
+  }
+  std::vector<double> pu((size_t)m * n), pv((size_t)m * n), d4(n);
+  for (int j = 0; j < m; ++j)
+    for (int k = 0; k < n; ++k) {
+      // factored: Pu = outer(u, d) exactly as ShiftParams.expand (lfmodel.py:259-262)
+      pu[(size_t)j * n + k] = factored ? D->u[j] * D->d[k] : D->pu[(size_t)j * n + k];
+      pv[(size_t)j * n + k] = factored ? D->v[j] * D->d[k] : D->pv[(size_t)j * n + k];
+    }
+  if (!finite_all(pu.data(), pu.size()) || !finite_all(pv.data(), pv.size()))
+    return fail(FDL_ERR_INVALID, "shift parameters must be finite");
+  for (int k = 0; k < n; ++k) d4[k] = std::pow(D->d[k], 4.0);
+
+  // apertures
+  bool pinhole_all = true, real_tables = true;
+  std::vector<int> vap(m, -1);
+  if (D->view_aperture) {
+    if (!D->s || !D->scale) return fail(FDL_ERR_INVALID, "wide-aperture views need s and scale");
+    for (int j = 0; j < m; ++j) {
+      vap[j] = D->view_aperture[j];
+      if (vap[j] >= D->n_apertures) return fail(FDL_ERR_INVALID, "aperture index out of range");
+      if (vap[j] >= 0) {
+        pinhole_all = false;
+        const fdl_aperture& a = D->apertures[vap[j]];
+        if (a.table_im) real_tables = false;
+      }
+    }
+  }
+
+  // mode
+  double dmax = 1.0;
+  for (int k = 0; k < n; ++k) dmax = std::max(dmax, std::fabs(D->d[k]));
+  bool sym_d = true;
+  for (int k = 0; k < n; ++k)
+    if (std::fabs(D->d[k] + D->d[n - 1 - k]) > 1e-12 * dmax) sym_d = false;
+  bool antisym = true;
+  for (int j = 0; j < m && antisym; ++j)
+    for (int k = 0; k < n; ++k) {
+      double a = pu[(size_t)j * n + k] + pu[(size_t)j * n + n - 1 - k];
+      double b = pv[(size_t)j * n + k] + pv[(size_t)j * n + n - 1 - k];
+      double sc = 1e-12 * std::max(1.0, std::fabs(pu[(size_t)j * n + k]) + std::fabs(pv[(size_t)j * n + k]));
+      if (std::fabs(a) > sc || std::fabs(b) > sc) {
+        antisym = false;
+        break;
+      }
+    }
+  bool zero_shift = true;
+  for (size_t e = 0; e < pu.size(); ++e)
+    if (pu[e] != 0.0 || pv[e] != 0.0) {
+      zero_shift = false;
+      break;
+    }
+  const bool ok1 = pinhole_all && sym_d && antisym;
+  const bool ok2 = zero_shift && real_tables;
+  int mode;
+  if (D->force_path == 1) {
+    if (!ok1) return fail(FDL_ERR_INVALID, "toeplitz-real path needs pinhole views and symmetric shifts");
+    mode = MODE_SYMREAL;
+  } else if (D->force_path == 2) {
+    if (!ok2) return fail(FDL_ERR_INVALID, "real-A path needs zero shifts and real apertures");
+    mode = MODE_REALA;
+  } else if (D->force_path == 3) {
+    mode = MODE_COMPLEX;
+  } else {
+    mode = ok1 ? MODE_SYMREAL : (ok2 ? MODE_REALA : MODE_COMPLEX);
+  }
+  *mode_out = mode;
+
+  SolveParams& p = P.p;
+  p.m = m;
+  p.n = n;
+  p.C = C;
+  p.Hp = D->Hp;
+  p.Wp = D->Wp;
+  p.Whp = D->Wp / 2 + 1;
+  p.nrows = D->nrows;
+  p.mode = mode;
+  p.h = n / 2;
+  if (mode == MODE_COMPLEX) {
+    p.N = 2 * n;
+    p.R = C;
+    p.rowsM = 2 * m;
+  } else {
+    p.N = n;
+    p.R = 2 * C;
+    p.rowsM = m;
+  }
+  if (p.N > 128 || p.R > 16) return fail(FDL_ERR_UNSUPPORTED, "layer/channel count beyond the K1 kernels");
+  p.lam = D->lam;
+  p.eps = D->eps;
+  p.spectra = reinterpret_cast<const float2*>(D->spectra_dev);
+  p.layers = reinterpret_cast<float2*>(D->layers_dev);
+  p.status = D->status_dev;
+  // uniform d (Toeplitz Gram) detection
+  p.uniform_d = 0;
+  p.delta = 0.0;
+  if (n >= 2) {
+    double delta = (D->d[n - 1] - D->d[0]) / (n - 1);
+    bool uni = true;
+    for (int k = 0; k < n; ++k)
+      if (std::fabs(D->d[k] - (D->d[0] + k * delta)) > 1e-12 * dmax) uni = false;
+    p.uniform_d = uni ? 1 : 0;
+    p.delta = delta;
+  }
+
+  Blob& B = P.blob;
+  P.o_rows = B.add(rows.data(), rows.size() * sizeof(int));
+  P.o_pu = B.add(pu.data(), pu.size() * sizeof(double));
+  P.o_pv = B.add(pv.data(), pv.size() * sizeof(double));
+  P.o_d = B.add(D->d, n * sizeof(double));
+  P.o_d4 = B.add(d4.data(), n * sizeof(double));
+  P.o_vap = B.add(vap.data(), m * sizeof(int));
+  std::vector<double> s(m, 0.0), sc(m, 1.0);
+  if (D->s)
+    for (int j = 0; j < m; ++j) s[j] = D->s[j];
+  if (D->scale)
+    for (int j = 0; j < m; ++j) sc[j] = D->scale[j];
+  P.o_s = B.add(s.data(), m * sizeof(double));
+  P.o_sc = B.add(sc.data(), m * sizeof(double));
+  const int nap = D->view_aperture ? D->n_apertures : 0;
+  P.o_aps = B.reserve(sizeof(DevAperture) * std::max(nap, 1));
+  for (int a = 0; a < nap; ++a) {
+    const fdl_aperture& ap = D->apertures[a];
+    if (ap.rows < 2 || ap.cols < 2 || !ap.table_re) return fail(FDL_ERR_INVALID, "aperture table needs >= 2x2 entries");
+    P.o_tab_re.push_back(B.add(ap.table_re, sizeof(double) * ap.rows * ap.cols));
+    P.o_tab_im.push_back(ap.table_im ? B.add(ap.table_im, sizeof(double) * ap.rows * ap.cols) : (size_t)-1);
+  }
+  P.o_cnt = B.reserve(sizeof(unsigned long long));
+  if (factored) {
+    // distinct u and v values -> per-axis phase tables (A_jk = px(u_j) py(v_j), construct.py:174)
+    auto distinct = [](const double* x, int m, std::vector<double>& vals, std::vector<int>& idx) {
+      idx.resize(m);
+      for (int j = 0; j < m; ++j) {
+        int f = -1;
+        for (size_t a = 0; a < vals.size(); ++a)
+          if (vals[a] == x[j]) {
+            f = (int)a;
+            break;
+          }
+        if (f < 0) {
+          vals.push_back(x[j]);
+          f = (int)vals.size() - 1;
+        }
+        idx[j] = f;
+      }
+    };
+    std::vector<double> uv, vv;
+    std::vector<int> ui, vi;
+    distinct(D->u, m, uv, ui);
+    distinct(D->v, m, vv, vi);
+    P.o_uidx = B.add(ui.data(), sizeof(int) * m);
+    P.o_vidx = B.add(vi.data(), sizeof(int) * m);
+    P.o_uval = B.add(uv.data(), sizeof(double) * uv.size());
+    P.o_vval = B.add(vv.data(), sizeof(double) * vv.size());
+    p.fast_nu = (int)uv.size();
+    p.fast_nv = (int)vv.size();
+    P.has_axes = true;
+  }
+  return FDL_OK;
+}
+
+void bind_solve(SolvePlan& P, const fdl_solve_desc* D, void* ws) {
+  SolveParams& p = P.p;
+  p.rows = at<int>(ws, P.o_rows);
+  p.pu = at<double>(ws, P.o_pu);
+  p.pv = at<double>(ws, P.o_pv);
+  p.d = at<double>(ws, P.o_d);
+  p.d4 = at<double>(ws, P.o_d4);
+  p.view_ap = D->view_aperture ? at<int>(ws, P.o_vap) : nullptr;
+  p.s = at<double>(ws, P.o_s);
+  p.scale = at<double>(ws, P.o_sc);
+  p.aps = at<DevAperture>(ws, P.o_aps);
+  if (P.has_axes) {
+    p.fast_u_idx = at<int>(ws, P.o_uidx);
+    p.fast_v_idx = at<int>(ws, P.o_vidx);
+    p.fast_u_val = at<double>(ws, P.o_uval);
+    p.fast_v_val = at<double>(ws, P.o_vval);
+  } else {
+    p.fast_u_idx = p.fast_v_idx = nullptr;
+    p.fast_u_val = p.fast_v_val = nullptr;
+  }
+  const int nap = (int)P.o_tab_re.size();
+  DevAperture* host_aps = reinterpret_cast<DevAperture*>(P.blob.bytes.data() + P.o_aps);
+  for (int a = 0; a < nap; ++a) {
+    const fdl_aperture& ap = D->apertures[a];
+    DevAperture da;
+    da.rows = ap.rows;
+    da.cols = ap.cols;
+    da.re = at<double>(ws, P.o_tab_re[a]);
+    da.im = ap.table_im ? at<double>(ws, P.o_tab_im[a]) : nullptr;
+    da.xi0_x = ap.xi0_x;
+    da.step_x = ap.step_x;
+    da.xi0_y = ap.xi0_y;
+    da.step_y = ap.step_y;
+    host_aps[a] = da;
+  }
+}
+
+__global__ void count_status_kernel(const signed char* st, long long n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    c += st[i] != 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// K2: conjugate-pair symmetrisation of the kx in {0, Wp/2} columns (construct.py:286-297)
+__global__ void symmetrize_kernel(float2* L, int planes, int nrows, int Whp, int Wp, const int* mirror) {
+  const int ncols = (Wp % 2 == 0) ? 2 : 1;
+  const long long total = (long long)planes * nrows * ncols;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int ci = (int)(idx % ncols);
+    long long r = idx / ncols;
+    int i = (int)(r % nrows);
+    long long pl = r / nrows;
+    int mi = mirror[i];
+    if (mi < i) continue;  // the pair is handled from its lower slab index
+    int kx = ci == 0 ? 0 : Wp / 2;
+    float2* base = L + pl * (long long)nrows * Whp;
+    float2 a = base[(size_t)i * Whp + kx], b = base[(size_t)mi * Whp + kx];
+    float2 na = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
+    base[(size_t)i * Whp + kx] = na;
+    if (mi != i) base[(size_t)mi * Whp + kx] = make_float2(na.x, -na.y);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 planning
+// ---------------------------------------------------------------------------
+struct RenderPlan {
+  Blob blob;
+  RenderParams p{};
+  size_t o_pu, o_pv, o_t, o_vap, o_aps, o_tabs, o_px, o_py;
+  std::vector<size_t> o_re, o_im;
+};
+
+int plan_render(const fdl_render_desc* D, RenderPlan& P) {
+  if (!D) return fail(FDL_ERR_INVALID, "null descriptor");
+  const int n = D->n, V = D->V;
+  if (n < 1 || D->C < 1 || D->Hp < 1 || D->Wp < 1 || V < 0) return fail(FDL_ERR_INVALID, "invalid render shape");
+  if (!D->pu || !D->pv) return fail(FDL_ERR_INVALID, "render needs per-(view, layer) shifts");
+  const size_t vn = (size_t)V * n;
+  if (!finite_all(D->pu, vn) || !finite_all(D->pv, vn)) return fail(FDL_ERR_INVALID, "shifts must be finite");
+  const int Whp = D->Wp / 2 + 1;
+  RenderParams& p = P.p;
+  p.n = n;
+  p.C = D->C;
+  p.Hp = D->Hp;
+  p.Wp = D->Wp;
+  p.Whp = Whp;
+  p.V = V;
+  p.layers = reinterpret_cast<const float2*>(D->layers_dev);
+  p.out = reinterpret_cast<float2*>(D->out_dev);
+  p.oob = reinterpret_cast<long long*>(D->oob_dev);
+  Blob& B = P.blob;
+  P.o_pu = B.add(D->pu, vn * sizeof(double));
+  P.o_pv = B.add(D->pv, vn * sizeof(double));
+  std::vector<double> t(vn, 0.0);
+  std::vector<int> vap(std::max(V, 1), -1);
+  const int nap = D->view_aperture ? D->n_apertures : 0;
+  if (D->view_aperture) {
+    if (!D->t) return fail(FDL_ERR_INVALID, "aperture renders need t = f (s - d)");
+    for (int v = 0; v < V; ++v) {
+      vap[v] = D->view_aperture[v];
+      if (vap[v] >= nap) return fail(FDL_ERR_INVALID, "aperture index out of range");
+    }
+    for (size_t e = 0; e < vn; ++e) t[e] = D->t[e];
+    if (!finite_all(t.data(), vn)) return fail(FDL_ERR_INVALID, "aperture scale must be finite");
+  }
+  P.o_t = B.add(t.data(), vn * sizeof(double));
+  P.o_vap = B.add(vap.data(), vap.size() * sizeof(int));
+  P.o_aps = B.reserve(sizeof(DevAperture) * std::max(nap, 1));
+  P.o_tabs = B.reserve(sizeof(RenderTable) * std::max(nap, 1));
+  for (int a = 0; a < nap; ++a) {
+    const fdl_aperture& ap = D->apertures[a];
+    if (ap.rows < 2 || ap.cols < 2 || !ap.table_re) return fail(FDL_ERR_INVALID, "aperture table needs >= 2x2 entries");
+    size_t cnt = (size_t)ap.rows * ap.cols;
+    std::vector<float> tmp(cnt);
+    for (size_t e = 0; e < cnt; ++e) tmp[e] = (float)ap.table_re[e];
+    P.o_re.push_back(B.add(tmp.data(), cnt * sizeof(float)));
+    if (ap.table_im) {
+      for (size_t e = 0; e < cnt; ++e) tmp[e] = (float)ap.table_im[e];
+      P.o_im.push_back(B.add(tmp.data(), cnt * sizeof(float)));
+    } else {
+      P.o_im.push_back((size_t)-1);
+    }
+  }
+  return FDL_OK;
+}
+
+size_t render_ws_bytes(const RenderPlan& P) {
+  const RenderParams& p = P.p;
+  return P.blob.size() + align256(sizeof(AxisFactor) * (size_t)p.V * p.n * p.Whp) +
+         align256(sizeof(AxisFactor) * (size_t)p.V * p.n * p.Hp);
+}
+
+void bind_render(RenderPlan& P, const fdl_render_desc* D, void* ws) {
+  RenderParams& p = P.p;
+  p.pu = at<double>(ws, P.o_pu);
+  p.pv = at<double>(ws, P.o_pv);
+  p.t = at<double>(ws, P.o_t);
+  p.view_ap = D->view_aperture ? at<int>(ws, P.o_vap) : nullptr;
+  p.aps = at<DevAperture>(ws, P.o_aps);
+  p.tables = at<RenderTable>(ws, P.o_tabs);
+  const int nap = (int)P.o_re.size();
+  DevAperture* haps = reinterpret_cast<DevAperture*>(P.blob.bytes.data() + P.o_aps);
+  RenderTable* htab = reinterpret_cast<RenderTable*>(P.blob.bytes.data() + P.o_tabs);
+  for (int a = 0; a < nap; ++a) {
+    const fdl_aperture& ap = D->apertures[a];
+    DevAperture da{};
+    da.rows = ap.rows;
+    da.cols = ap.cols;
+    da.xi0_x = ap.xi0_x;
+    da.step_x = ap.step_x;
+    da.xi0_y = ap.xi0_y;
+    da.step_y = ap.step_y;
+    haps[a] = da;
+    RenderTable rt;
+    rt.rows = ap.rows;
+    rt.cols = ap.cols;
+    rt.re = at<float>(ws, P.o_re[a]);
+    rt.im = P.o_im[a] == (size_t)-1 ? nullptr : at<float>(ws, P.o_im[a]);
+    htab[a] = rt;
+  }
+  char* base = reinterpret_cast<char*>(ws) + P.blob.size();
+  p.px = reinterpret_cast<AxisFactor*>(base);
+  p.py = reinterpret_cast<AxisFactor*>(base + align256(sizeof(AxisFactor) * (size_t)p.V * p.n * p.Whp));
+}
+
+}  // namespace
+}  // namespace fdl
+
+// =============================================================================
+// extern "C"
+// =============================================================================
+using namespace fdl;
+
+extern "C" {
+
+int fdl_version(void) { return 100; }
+
+int fdl_selftest(double* max_err) {
+  double e = 0;
+  int rc = selftest_dmma(nullptr, &e);
+  if (max_err) *max_err = e;
+  if (rc) return rc;
+  return e <= 1e-12 ? FDL_OK : fail(FDL_ERR_CUDA, "DMMA fragment layout self-test failed");
+}
+
+const char* fdl_last_error(void) { return t_error.c_str(); }
+
+size_t fdl_views_to_spectra_workspace(int32_t m, int32_t H, int32_t W, int32_t C, int32_t pad) {
+  size_t b = 0;
+  if (m < 1 || H < 1 || W < 1 || C < 1 || pad < 0) return 0;
+  if (views_to_spectra_ws(m, H, W, C, pad, &b)) return 0;
+  return b;
+}
+
+int fdl_views_to_spectra(const float* views_dev, int32_t m, int32_t H, int32_t W, int32_t C, int32_t pad,
+                         fdl_c64* spectra_dev, double* view_sumsq_dev, void* workspace_dev, size_t workspace_bytes,
+                         void* stream) {
+  if (m < 1 || H < 1 || W < 1 || C < 1 || pad < 0) return fail(FDL_ERR_INVALID, "invalid view stack shape");
+  if (!views_dev || !spectra_dev) return fail(FDL_ERR_INVALID, "null buffer");
+  return views_to_spectra(views_dev, m, H, W, C, pad, spectra_dev, view_sumsq_dev, workspace_dev, workspace_bytes,
+                          as_stream(stream));
+}
+
+int fdl_gather_rows(const fdl_c64* src_dev, int32_t m, int32_t C, int32_t Hp, int32_t Whp, const int32_t* rows_dev,
+                    int32_t nrows, fdl_c64* dst_dev, void* stream) {
+  if (m < 0 || C < 1 || Hp < 1 || Whp < 1 || nrows < 0) return fail(FDL_ERR_INVALID, "invalid gather shape");
+  return gather_rows(src_dev, m, C, Hp, Whp, rows_dev, nrows, dst_dev, as_stream(stream));
+}
+
+size_t fdl_solve_bins_workspace(const fdl_solve_desc* desc) {
+  SolvePlan P;
+  int mode;
+  if (plan_solve(desc, P, &mode)) return 0;
+  return P.blob.size();
+}
+
+int fdl_solve_path(const fdl_solve_desc* desc) {
+  SolvePlan P;
+  int mode;
+  int rc = plan_solve(desc, P, &mode);
+  return rc ? rc : mode;
+}
+
+int fdl_solve_bins(const fdl_solve_desc* desc, void* workspace_dev, size_t workspace_bytes, int32_t* n_breakdown,
+                   void* stream) {
+  SolvePlan P;
+  int mode;
+  int rc = plan_solve(desc, P, &mode);
+  if (rc) return rc;
+  if (workspace_bytes < P.blob.size() || !workspace_dev) return fail(FDL_ERR_INVALID, "workspace too small for fdl_solve_bins");
+  if (!desc->spectra_dev || !desc->layers_dev) return fail(FDL_ERR_INVALID, "null spectra/layers buffer");
+  cudaStream_t st = as_stream(stream);
+  bind_solve(P, desc, workspace_dev);
+  unsigned long long zero = 0;
+  std::memcpy(P.blob.bytes.data() + P.o_cnt, &zero, sizeof(zero));
+  rc = upload(P.blob, workspace_dev, st);
+  if (rc) return rc;
+  if (desc->nrows == 0) {
+    if (n_breakdown) *n_breakdown = 0;
+    return FDL_OK;
+  }
+  bool handled = false;
+  if (desc->force_path >= 0 && desc->force_path != 4) rc = k1_fast_launch(P.p, st, &handled);
+  if (rc) return rc;
+  if (!handled) {
+    rc = k1_generic_launch(P.p, st);
+    if (rc) return rc;
+  }
+  if (n_breakdown) {
+    *n_breakdown = 0;
+    if (desc->status_dev) {
+      unsigned long long* cnt = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(workspace_dev) + P.o_cnt);
+      long long nb = (long long)desc->nrows * P.p.Whp;
+      count_status_kernel<<<148, 256, 0, st>>>(desc->status_dev, nb, cnt);
+      FDL_LAUNCH_CHECK("count_status_kernel");
+      unsigned long long h = 0;
+      FDL_CUDA_CHECK(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+      FDL_CUDA_CHECK(cudaStreamSynchronize(st));
+      *n_breakdown = (int32_t)h;
+    }
+  }
+  return FDL_OK;
+}
+
+int fdl_symmetrize(fdl_c64* layers_dev, int32_t n, int32_t C, int32_t Hp, int32_t Wp, int32_t nrows,
+                   const int32_t* rows, const int32_t* mirror, void* stream) {
+  if (n < 1 || C < 1 || Hp < 1 || Wp < 1 || nrows < 0 || nrows > Hp) return fail(FDL_ERR_INVALID, "invalid layer shape");
+  if (nrows == 0) return FDL_OK;
+  std::vector<int> mir(nrows);
+  for (int i = 0; i < nrows; ++i) {
+    int r = rows ? rows[i] : i;
+    if (r < 0 || r >= Hp) return fail(FDL_ERR_INVALID, "slab row out of range");
+    if (mirror) {
+      mir[i] = mirror[i];
+    } else {
+      if (nrows != Hp || rows) return fail(FDL_ERR_INVALID, "a partial slab needs the mirror map");
+      mir[i] = (Hp - i) % Hp;
+    }
+    if (mir[i] < 0 || mir[i] >= nrows) return fail(FDL_ERR_INVALID, "mirror row outside the slab");
+  }
+  // device copy of the mirror map: tiny, goes through the staging ring
+  // (workspace-free API: a per-thread device scratch)
+  static thread_local int* t_mirror = nullptr;
+  static thread_local size_t t_mirror_cap = 0;
+  if (t_mirror_cap < (size_t)nrows) {
+    if (t_mirror) cudaFree(t_mirror);
+    FDL_CUDA_CHECK(cudaMalloc(&t_mirror, sizeof(int) * nrows));
+    t_mirror_cap = nrows;
+  }
+  Blob b;
+  b.add(mir.data(), sizeof(int) * nrows);
+  cudaStream_t st = as_stream(stream);
+  int rc = upload(b, t_mirror, st);
+  if (rc) return rc;
+  const int Whp = Wp / 2 + 1;
+  long long total = (long long)n * C * nrows * ((Wp % 2 == 0) ? 2 : 1);
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  symmetrize_kernel<<<std::max(blocks, 1), 256, 0, st>>>(reinterpret_cast<float2*>(layers_dev), n * C, nrows, Whp, Wp,
+                                                          t_mirror);
+  FDL_LAUNCH_CHECK("symmetrize_kernel");
+  return FDL_OK;
+}
+
+size_t fdl_render_workspace(const fdl_render_desc* desc) {
+  RenderPlan P;
+  if (plan_render(desc, P)) return 0;
+  return render_ws_bytes(P);
+}
+
+int fdl_render_spectra(const fdl_render_desc* desc, void* workspace_dev, size_t workspace_bytes, void* stream) {
+  RenderPlan P;
+  int rc = plan_render(desc, P);
+  if (rc) return rc;
+  if (workspace_bytes < render_ws_bytes(P) || !workspace_dev) return fail(FDL_ERR_INVALID, "workspace too small for fdl_render_spectra");
+  if (!desc->layers_dev || !desc->out_dev) return fail(FDL_ERR_INVALID, "null layers/out buffer");
+  cudaStream_t st = as_stream(stream);
+  bind_render(P, desc, workspace_dev);
+  rc = upload(P.blob, workspace_dev, st);
+  if (rc) return rc;
+  if (desc->oob_dev && desc->V > 0) FDL_CUDA_CHECK(cudaMemsetAsync(desc->oob_dev, 0, sizeof(int64_t) * desc->V, st));
+  return render_launch(P.p, st);
+}
+
+size_t fdl_spectra_to_images_workspace(int32_t V, int32_t C, int32_t Hp, int32_t Wp) {
+  size_t b = 0;
+  if (V < 1 || C < 1 || Hp < 1 || Wp < 1) return 0;
+  if (spectra_to_images_ws(V, C, Hp, Wp, &b)) return 0;
+  return b;
+}
+
+int fdl_spectra_to_images(fdl_c64* spectra_dev, int32_t V, int32_t C, int32_t Hp, int32_t Wp, int32_t pad,
+                          int32_t Ho, int32_t Wo, int32_t srgb, float* images_dev, void* workspace_dev,
+                          size_t workspace_bytes, void* stream) {
+  if (V < 0 || C < 1 || Hp < 1 || Wp < 1 || Ho < 1 || Wo < 1) return fail(FDL_ERR_INVALID, "invalid image shape");
+  if (V == 0) return FDL_OK;
+  return spectra_to_images(spectra_dev, V, C, Hp, Wp, pad, Ho, Wo, srgb, images_dev, workspace_dev, workspace_bytes,
+                           as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,254 @@
+// K0: zero-pad + batched R2C + per-view sum |b|^2  (construct.py:250-266).
+// K4: Hermitian projection of self-conjugate columns + C2R + crop + sRGB
+//     (spectra.py:202-208, render.py:210-225).
+//
+// Both are HBM-bound streaming kernels around cuFFT.  Plans are cached per
+// host thread (cuFFT plans are not safe to share between concurrent callers)
+// and never allocate: their work area comes from the caller's workspace.
+#include <cufft.h>
+
+#include <map>
+#include <tuple>
+
+#include "common.cuh"
+
+namespace fdl {
+
+namespace {
+
+struct PlanKey {
+  int h, w, batch, type;
+  bool operator<(const PlanKey& o) const {
+    return std::tie(h, w, batch, type) < std::tie(o.h, o.w, o.batch, o.type);
+  }
+};
+
+struct Plan {
+  cufftHandle handle = 0;
+  size_t work = 0;
+};
+
+thread_local std::map<PlanKey, Plan> t_plans;
+
+// type 0: R2C (real input H x W -> H x (W/2+1)), 1: C2R
+int get_plan(int h, int w, int batch, int type, Plan** out) {
+  PlanKey key{h, w, batch, type};
+  auto it = t_plans.find(key);
+  if (it != t_plans.end()) {
+    *out = &it->second;
+    return FDL_OK;
+  }
+  Plan p;
+  if (cufftCreate(&p.handle) != CUFFT_SUCCESS) return fail(FDL_ERR_CUDA, "cufftCreate failed");
+  cufftSetAutoAllocation(p.handle, 0);
+  int n[2] = {h, w};
+  int whp = w / 2 + 1;
+  cufftResult r;
+  if (type == 0) {
+    int inembed[2] = {h, w}, onembed[2] = {h, whp};
+    r = cufftMakePlanMany(p.handle, 2, n, inembed, 1, h * w, onembed, 1, h * whp, CUFFT_R2C, batch, &p.work);
+  } else {
+    int inembed[2] = {h, whp}, onembed[2] = {h, w};
+    r = cufftMakePlanMany(p.handle, 2, n, inembed, 1, h * whp, onembed, 1, h * w, CUFFT_C2R, batch, &p.work);
+  }
+  if (r != CUFFT_SUCCESS) {
+    cufftDestroy(p.handle);
+    return fail(FDL_ERR_CUDA, "cufftMakePlanMany failed (" + std::to_string((int)r) + ")");
+  }
+  auto res = t_plans.emplace(key, p);
+  *out = &res.first->second;
+  return FDL_OK;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// views (m,H,W,C) -> padded planar (m,C,Hp,Wp)
+__global__ void pack_pad_kernel(const float* __restrict__ views, int m, int H, int W, int C, int pad,
+                                float* __restrict__ out) {
+  const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+  const size_t total = (size_t)m * C * Hp * Wp;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    int x = (int)(idx % Wp);
+    size_t r = idx / Wp;
+    int y = (int)(r % Hp);
+    r /= Hp;
+    int c = (int)(r % C);
+    int j = (int)(r / C);
+    int xs = x - pad, ys = y - pad;
+    float v = 0.f;
+    if (xs >= 0 && xs < W && ys >= 0 && ys < H) v = __ldg(views + (((size_t)j * H + ys) * W + xs) * C + c);
+    out[idx] = v;
+  }
+}
+
+// one block per view: sum over (C, Hp, Whp) of |b|^2 in float64, fixed order
+__global__ void view_sumsq_kernel(const float2* __restrict__ spec, size_t per_view, double* __restrict__ out) {
+  const float2* p = spec + (size_t)blockIdx.x * per_view;
+  double acc = 0.0;
+  for (size_t i = threadIdx.x; i < per_view; i += blockDim.x) {
+    float2 b = p[i];
+    acc += (double)b.x * b.x + (double)b.y * b.y;
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) out[blockIdx.x] = v;
+  }
+}
+
+__global__ void gather_rows_kernel(const float2* __restrict__ src, int planes, int Hp, int Whp,
+                                   const int* __restrict__ rows, int nrows, float2* __restrict__ dst) {
+  const size_t total = (size_t)planes * nrows * Whp;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    int kx = (int)(idx % Whp);
+    size_t r = idx / Whp;
+    int i = (int)(r % nrows);
+    size_t pl = r / nrows;
+    dst[idx] = src[(pl * Hp + rows[i]) * Whp + kx];
+  }
+}
+
+// Project the kx = 0 (and even-W Nyquist) columns onto their Hermitian part,
+// v <- (v + conj(v[flip_y])) / 2: exactly the input numpy's irfft2 inverts
+// (its c2r pass drops the imaginary part of those columns after the y pass).
+__global__ void hermitize_cols_kernel(float2* __restrict__ spec, int planes, int Hp, int Wp) {
+  const int Whp = Wp / 2 + 1;
+  const int ncols = (Wp % 2 == 0) ? 2 : 1;
+  const int half = Hp / 2 + 1;  // rows 0..Hp/2 pair with Hp-row
+  const size_t total = (size_t)planes * ncols * half;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    int ky = (int)(idx % half);
+    size_t r = idx / half;
+    int ci = (int)(r % ncols);
+    size_t pl = r / ncols;
+    int kx = ci == 0 ? 0 : Wp / 2;
+    int my = (Hp - ky) % Hp;
+    float2* base = spec + pl * (size_t)Hp * Whp;
+    float2 a = base[(size_t)ky * Whp + kx];
+    float2 b = base[(size_t)my * Whp + kx];
+    float2 na = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
+    float2 nb = make_float2(na.x, -na.y);
+    base[(size_t)ky * Whp + kx] = na;
+    if (my != ky) base[(size_t)my * Whp + kx] = nb;
+  }
+}
+
+__device__ inline float srgb_enc(float x) {
+  // render.py:45-48 (negative inputs clamp to 0)
+  x = fmaxf(x, 0.f);
+  return x <= 0.0031308f ? x * 12.92f : 1.055f * powf(x, 1.0f / 2.4f) - 0.055f;
+}
+
+// (V, C, Hp, Wp) real planes scaled by 1/(Hp Wp) -> (V, Ho, Wo, C) cropped
+__global__ void crop_kernel(const float* __restrict__ planes, int V, int C, int Hp, int Wp, int pad, int Ho,
+                            int Wo, int srgb, float scale, float* __restrict__ out) {
+  const size_t total = (size_t)V * Ho * Wo * C;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    int c = (int)(idx % C);
+    size_t r = idx / C;
+    int x = (int)(r % Wo);
+    r /= Wo;
+    int y = (int)(r % Ho);
+    int v = (int)(r / Ho);
+    float val = planes[(((size_t)v * C + c) * Hp + (y + pad)) * Wp + (x + pad)] * scale;
+    if (srgb) val = srgb_enc(val);
+    out[idx] = val;
+  }
+}
+
+inline int grid_for(size_t total, int threads) {
+  size_t b = (total + threads - 1) / threads;
+  int sms = 148;
+  size_t cap = (size_t)sms * 16;
+  return (int)(b < cap ? (b > 0 ? b : 1) : cap);
+}
+
+}  // namespace
+
+int views_to_spectra_ws(int m, int H, int W, int C, int pad, size_t* bytes) {
+  const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+  Plan* plan;
+  int rc = get_plan(Hp, Wp, m * C, 0, &plan);
+  if (rc) return rc;
+  *bytes = align256((size_t)m * C * Hp * Wp * sizeof(float)) + align256(plan->work);
+  return FDL_OK;
+}
+
+int views_to_spectra(const float* views, int m, int H, int W, int C, int pad, fdl_c64* spectra,
+                     double* view_sumsq, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int Hp = H + 2 * pad, Wp = W + 2 * pad, Whp = Wp / 2 + 1;
+  size_t need;
+  int rc = views_to_spectra_ws(m, H, W, C, pad, &need);
+  if (rc) return rc;
+  if (ws_bytes < need || (need && !ws)) return fail(FDL_ERR_INVALID, "workspace too small for fdl_views_to_spectra");
+  Plan* plan;
+  get_plan(Hp, Wp, m * C, 0, &plan);
+  float* padded = reinterpret_cast<float*>(ws);
+  void* fft_work = reinterpret_cast<char*>(ws) + align256((size_t)m * C * Hp * Wp * sizeof(float));
+  size_t total = (size_t)m * C * Hp * Wp;
+  pack_pad_kernel<<<grid_for(total, 256), 256, 0, st>>>(views, m, H, W, C, pad, padded);
+  FDL_LAUNCH_CHECK("pack_pad_kernel");
+  if (cufftSetStream(plan->handle, st) != CUFFT_SUCCESS) return fail(FDL_ERR_CUDA, "cufftSetStream");
+  if (cufftSetWorkArea(plan->handle, fft_work) != CUFFT_SUCCESS) return fail(FDL_ERR_CUDA, "cufftSetWorkArea");
+  if (cufftExecR2C(plan->handle, padded, reinterpret_cast<cufftComplex*>(spectra)) != CUFFT_SUCCESS)
+    return fail(FDL_ERR_CUDA, "cufftExecR2C failed");
+  if (view_sumsq) {
+    view_sumsq_kernel<<<m, 1024, 0, st>>>(reinterpret_cast<const float2*>(spectra), (size_t)C * Hp * Whp,
+                                          view_sumsq);
+    FDL_LAUNCH_CHECK("view_sumsq_kernel");
+  }
+  return FDL_OK;
+}
+
+int gather_rows(const fdl_c64* src, int m, int C, int Hp, int Whp, const int* rows_dev, int nrows, fdl_c64* dst,
+                cudaStream_t st) {
+  size_t total = (size_t)m * C * nrows * Whp;
+  if (total == 0) return FDL_OK;
+  gather_rows_kernel<<<grid_for(total, 256), 256, 0, st>>>(reinterpret_cast<const float2*>(src), m * C, Hp, Whp,
+                                                           rows_dev, nrows, reinterpret_cast<float2*>(dst));
+  FDL_LAUNCH_CHECK("gather_rows_kernel");
+  return FDL_OK;
+}
+
+int spectra_to_images_ws(int V, int C, int Hp, int Wp, size_t* bytes) {
+  Plan* plan;
+  int rc = get_plan(Hp, Wp, V * C, 1, &plan);
+  if (rc) return rc;
+  *bytes = align256((size_t)V * C * Hp * Wp * sizeof(float)) + align256(plan->work);
+  return FDL_OK;
+}
+
+int spectra_to_images(fdl_c64* spectra, int V, int C, int Hp, int Wp, int pad, int Ho, int Wo, int srgb,
+                      float* images, void* ws, size_t ws_bytes, cudaStream_t st) {
+  size_t need;
+  int rc = spectra_to_images_ws(V, C, Hp, Wp, &need);
+  if (rc) return rc;
+  if (ws_bytes < need || !ws) return fail(FDL_ERR_INVALID, "workspace too small for fdl_spectra_to_images");
+  if (pad < 0 || Ho + pad > Hp || Wo + pad > Wp) return fail(FDL_ERR_INVALID, "crop window outside the grid");
+  Plan* plan;
+  get_plan(Hp, Wp, V * C, 1, &plan);
+  float* planes = reinterpret_cast<float*>(ws);
+  void* fft_work = reinterpret_cast<char*>(ws) + align256((size_t)V * C * Hp * Wp * sizeof(float));
+  size_t hn = (size_t)V * C * ((Wp % 2 == 0) ? 2 : 1) * (Hp / 2 + 1);
+  hermitize_cols_kernel<<<grid_for(hn, 256), 256, 0, st>>>(reinterpret_cast<float2*>(spectra), V * C, Hp, Wp);
+  FDL_LAUNCH_CHECK("hermitize_cols_kernel");
+  if (cufftSetStream(plan->handle, st) != CUFFT_SUCCESS) return fail(FDL_ERR_CUDA, "cufftSetStream");
+  if (cufftSetWorkArea(plan->handle, fft_work) != CUFFT_SUCCESS) return fail(FDL_ERR_CUDA, "cufftSetWorkArea");
+  if (cufftExecC2R(plan->handle, reinterpret_cast<cufftComplex*>(spectra), planes) != CUFFT_SUCCESS)
+    return fail(FDL_ERR_CUDA, "cufftExecC2R failed");
+  size_t total = (size_t)V * Ho * Wo * C;
+  float scale = (float)(1.0 / ((double)Hp * (double)Wp));
+  crop_kernel<<<grid_for(total, 256), 256, 0, st>>>(planes, V, C, Hp, Wp, pad, Ho, Wo, srgb, scale, images);
+  FDL_LAUNCH_CHECK("crop_kernel");
+  return FDL_OK;
+}
+
+}  // namespace fdl

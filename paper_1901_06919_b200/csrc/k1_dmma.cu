@@ -1,0 +1,507 @@
+// K1 fast path: one warp per frequency bin, everything on the FP64 tensor
+// cores (DMMA m8n8k4, measured 36.9 TF/s on B200 vs 34.2 TF/s for DFMA) with
+// the normal matrix resident in registers.
+//
+// Per bin (k1_solve.cuh explains the real re-writes):
+//   1. rows of the real design matrix M (and of B) are generated per lane
+//      directly in DMMA fragment layout, 4 rows per k-step;
+//        RHS_I += M_I^T B           (NB DMMAs / k-step)
+//        G_IJ  += M_I^T M_J, J <= I (NB(NB+1)/2 DMMAs / k-step)
+//   2. G += lam diag(reg') (reg' = reg of the layer pair; padding -> identity);
+//   3. blocked right-looking Cholesky, block 8, all blocks in registers as
+//      accumulator fragments: per step K the 8x8 diagonal block is factored
+//      and inverted by 8 lanes (W = L_KK^-1), the panel is L_IK = G_IK W^T
+//      (DMMA), the trailing update G_IJ -= L_IK L_JK^T (DMMA) and the forward
+//      substitution y_K = W r_K, r_I -= L_IK y_K (DMMA) run interleaved;
+//   4. backward substitution x_K = W^T (y_K - sum_{I>K} L_IK^T x_I) (DMMA);
+//   5. x mapped back to complex layer coefficients, written as complex64.
+//
+// DMMA fragment layouts (m8n8k4, row.col, f64; lane l, q = l>>2, t = l&3):
+//   A (8x4): A[q][t]   B (4x8): B[t][q]   C (8x8): C[q][2t], C[q][2t+1]
+// (checked on the device by fdl_selftest).
+#include "k1_solve.cuh"
+
+namespace fdl {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int WARPS = 8;  // bins (consecutive kx of one row) per CTA
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// accumulator fragment -> A-fragment pair (C[q][t], C[q][4+t]) of the same block
+__device__ __forceinline__ void c_to_a(const double (&c)[2], double& a0, double& a1, int lane) {
+  const int q = lane >> 2, t = lane & 3;
+  const int s0 = (q << 2) + (t >> 1), s1 = s0 + 2;
+  const double x0 = __shfl_sync(FULL, c[0], s0), x1 = __shfl_sync(FULL, c[1], s0);
+  const double y0 = __shfl_sync(FULL, c[0], s1), y1 = __shfl_sync(FULL, c[1], s1);
+  a0 = (t & 1) ? x1 : x0;
+  a1 = (t & 1) ? y1 : y0;
+}
+
+// accumulator fragment -> A-fragment pair of the TRANSPOSED block (C[t][q], C[4+t][q])
+__device__ __forceinline__ void c_to_at(const double (&c)[2], double& a0, double& a1, int lane) {
+  const int q = lane >> 2, t = lane & 3;
+  const int s0 = (t << 2) + (q >> 1), s1 = s0 + 16;
+  const double x0 = __shfl_sync(FULL, c[0], s0), x1 = __shfl_sync(FULL, c[1], s0);
+  const double y0 = __shfl_sync(FULL, c[0], s1), y1 = __shfl_sync(FULL, c[1], s1);
+  a0 = (q & 1) ? x1 : x0;
+  a1 = (q & 1) ? y1 : y0;
+}
+
+__device__ __forceinline__ void store_c(double* S, const double (&c)[2], int lane) {
+  const int q = lane >> 2, t = lane & 3;
+  S[q * 8 + 2 * t] = c[0];
+  S[q * 8 + 2 * t + 1] = c[1];
+}
+
+struct FastParams {
+  const int* u_idx;     // (m) index of u_j among the distinct u values
+  const int* v_idx;     // (m)
+  const double* u_val;  // (nu)
+  const double* v_val;  // (nv)
+  int nu, nv;
+  int H8;               // columns per cos/sin half, multiple of 8 (mode 1)
+  int hw;               // phase-table width: h + (n odd)
+};
+
+__host__ __device__ constexpr int blk(int I, int J) { return I * (I + 1) / 2 + J; }
+
+template <int NB, int MODE, int ODD>
+__global__ void __launch_bounds__(WARPS * 32, 1) k1_fast_kernel(SolveParams p, FastParams f) {
+  constexpr int NBc = (NB - ODD) / 2;  // blocks of the cos half (= of the sin half), mode 1
+  constexpr int NBLK = NB * (NB + 1) / 2;
+  constexpr int NP = NB * 8;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane >> 2, t = lane & 3;
+  const int i = blockIdx.y;
+  const int kx = blockIdx.x * WARPS + warp;
+  const int ky = p.rows[i];
+  const double ox = omega_x_label(kx, p.Wp), oy = omega_y_label(ky, p.Hp);
+  const bool nyq_x = (p.Wp % 2 == 0) && kx == p.Wp / 2;
+  const bool nyq_y = (p.Hp % 2 == 0) && ky == p.Hp / 2;
+
+  // shared layout: [PY: nv*hw complex] then per warp [PX: nu*hw complex | S 64 | T 64 | Wst NB*64 | X NP*8]
+  double* PY = smem;
+  const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hw : 0;
+  const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hw : 0;
+  const int per_warp = px_words + 64 + 64 + NB * 64 + NP * 8;
+  double* base = smem + py_words + warp * per_warp;
+  double* PX = base;
+  double* S = PX + px_words;
+  double* T = S + 64;
+  double* Wst = T + 64;
+  double* X = Wst + NB * 64;
+
+  if (MODE == MODE_SYMREAL) {
+    // exp(2 pi i fl(v d_p) wy) per distinct v, shared by the CTA's bins (same row)
+    for (int e = threadIdx.x; e < f.nv * f.hw; e += blockDim.x) {
+      const int iv = e / f.hw, pp = e % f.hw;
+      cd ph = axis_phase(f.v_val[iv] * p.d[pp], oy, nyq_y);
+      PY[2 * e] = ph.re;
+      PY[2 * e + 1] = ph.im;
+    }
+  }
+  __syncthreads();
+  if (kx >= p.Whp) return;  // warp-uniform; no block barriers below
+
+  if (MODE == MODE_SYMREAL) {
+    for (int e = lane; e < f.nu * f.hw; e += 32) {
+      const int iu = e / f.hw, pp = e % f.hw;
+      cd ph = axis_phase(f.u_val[iu] * p.d[pp], ox, nyq_x);
+      PX[2 * e] = ph.re;
+      PX[2 * e + 1] = ph.im;
+    }
+    __syncwarp();
+  }
+
+  double g[NBLK][2];
+  double r[NB][2];
+#pragma unroll
+  for (int b = 0; b < NBLK; ++b) g[b][0] = g[b][1] = 0.0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) r[b][0] = r[b][1] = 0.0;
+
+  const size_t plane = (size_t)p.nrows * p.Whp;
+  const size_t boff = (size_t)i * p.Whp + kx;
+  const int h = p.h;
+
+  // ---------------------------------------------------------------- 1. Gram + RHS
+  for (int r0 = 0; r0 < p.m; r0 += 4) {
+    const int j = r0 + t;
+    double mf[NB];
+    double bf = 0.0;
+    if (j < p.m) {
+      if (q < 2 * p.C) {
+        const float2 b = p.spectra[((size_t)j * p.C + (q >> 1)) * plane + boff];
+        bf = (q & 1) ? (double)b.y : (double)b.x;
+      }
+      if (MODE == MODE_SYMREAL) {
+        const double* pxr = PX + 2 * f.u_idx[j] * f.hw;
+        const double* pyr = PY + 2 * f.v_idx[j] * f.hw;
+#pragma unroll
+        for (int I = 0; I < NB; ++I) mf[I] = 0.0;
+#pragma unroll
+        for (int I = 0; I < NB; ++I) {
+          if (I < NBc) {
+            const int pp = I * 8 + q;
+            if (pp < h) {
+              cd a = cmul_rn(cd{pxr[2 * pp], pxr[2 * pp + 1]}, cd{pyr[2 * pp], pyr[2 * pp + 1]});
+              mf[I] = M_SQRT2 * a.re;
+              mf[I + NBc] = -M_SQRT2 * a.im;
+            }
+          }
+        }
+        if (ODD && q == 0) {
+          cd a = cmul_rn(cd{pxr[2 * h], pxr[2 * h + 1]}, cd{pyr[2 * h], pyr[2 * h + 1]});
+          mf[NB - 1] = a.re;
+        }
+      } else {  // MODE_REALA: A_jk = psi_j(t_jk wx, t_jk wy) (all shifts are zero)
+        const int ai = p.view_ap ? p.view_ap[j] : -1;
+#pragma unroll
+        for (int I = 0; I < NB; ++I) {
+          const int k = I * 8 + q;
+          double v = 0.0;
+          if (k < p.n) {
+            if (ai < 0) {
+              v = 1.0;
+            } else {
+              const double tt = __dmul_rn(p.scale[j], __dsub_rn(p.s[j], p.d[k]));
+              v = aperture_eval(p.aps[ai], __dmul_rn(tt, ox), __dmul_rn(tt, oy)).re;
+            }
+          }
+          mf[I] = v;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int I = 0; I < NB; ++I) mf[I] = 0.0;
+    }
+#pragma unroll
+    for (int I = 0; I < NB; ++I) dmma(r[I], mf[I], bf);
+#pragma unroll
+    for (int I = 0; I < NB; ++I)
+#pragma unroll
+      for (int J = 0; J <= I; ++J) dmma(g[blk(I, J)], mf[I], mf[J]);
+  }
+
+  // ---------------------------------------------------------------- 2. + lam reg'
+  {
+    // reference rounding: ((wx^2 + wy^2)^2 * d^4 + eps), G += lam * reg (construct.py:283,194)
+    const double osq = __dadd_rn(__dmul_rn(ox, ox), __dmul_rn(oy, oy));
+    const double w4 = __dmul_rn(osq, osq);
+#pragma unroll
+    for (int I = 0; I < NB; ++I) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int rr = q, cc = 2 * t + e;
+        if (rr != cc) continue;
+        const int col = I * 8 + rr;
+        int k0 = -1, k1 = -1;
+        if (MODE == MODE_SYMREAL) {
+          const int H8 = f.H8;
+          if (col < H8) {
+            if (col < h) k0 = col;
+          } else if (col < 2 * H8) {
+            if (col - H8 < h) k0 = col - H8;
+          } else if (col == 2 * H8 && (p.n & 1)) {
+            k0 = h;
+          }
+          if (k0 >= 0 && k0 < h) k1 = p.n - 1 - k0;
+        } else {
+          if (col < p.n) k0 = col;
+        }
+        double add;
+        if (k0 < 0) {
+          add = 1.0;  // padding column: identity
+        } else {
+          double rg = __dadd_rn(__dmul_rn(w4, p.d4[k0]), p.eps);
+          if (k1 >= 0) rg = 0.5 * __dadd_rn(rg, __dadd_rn(__dmul_rn(w4, p.d4[k1]), p.eps));
+          add = p.lam > 0.0 ? __dmul_rn(p.lam, rg) : 0.0;
+        }
+        g[blk(I, I)][e] = __dadd_rn(g[blk(I, I)][e], add);
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- 3. Cholesky + forward
+  bool ok = true;
+#pragma unroll
+  for (int K = 0; K < NB; ++K) {
+    // (a) factor + invert the diagonal block with lanes 0..7 (lane = row)
+    store_c(S, g[blk(K, K)], lane);
+    __syncwarp();
+    double a[8];
+    bool lok = true;
+    if (lane < 8) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) a[c] = S[lane * 8 + c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) a[c] = (c == 0) ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double akk = __shfl_sync(FULL, a[k], k);
+      const bool good = (akk > 0.0) && isfinite(akk);
+      lok = lok && good;
+      const double lkk = sqrt(good ? akk : 1.0);
+      const double inv = 1.0 / lkk;
+      if (lane == k) a[k] = lkk;
+      if (lane > k) a[k] *= inv;
+#pragma unroll
+      for (int c = k + 1; c < 8; ++c) {
+        const double lck = __shfl_sync(FULL, a[k], c);
+        if (lane >= c) a[c] = fma(-a[k], lck, a[c]);
+      }
+    }
+    ok = __all_sync(FULL, lok) && ok;
+    __syncwarp();
+    if (lane < 8) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) S[lane * 8 + c] = (c <= lane) ? a[c] : 0.0;
+    }
+    __syncwarp();
+    if (lane < 8) {
+      // column `lane` of W = L^-1 by forward substitution
+      const int c = lane;
+      double w[8];
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) {
+        double acc = (rr == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < rr; ++k) acc = fma(-S[rr * 8 + k], w[k], acc);
+        w[rr] = (rr >= c) ? acc / S[rr * 8 + rr] : 0.0;
+      }
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) Wst[K * 64 + rr * 8 + c] = w[rr];
+    }
+    __syncwarp();
+    const double* Wk = Wst + K * 64;
+    // A-fragment of W (= B-fragment of W^T): W[q][t], W[q][4+t]
+    const double wa0 = Wk[q * 8 + t], wa1 = Wk[q * 8 + 4 + t];
+
+    // (b) panel L_IK = G_IK W^T, kept in place (accumulator layout) and as A-fragments
+    double lf[NB][2];
+#pragma unroll
+    for (int I = K + 1; I < NB; ++I) {
+      double a0, a1;
+      c_to_a(g[blk(I, K)], a0, a1, lane);
+      double d[2] = {0.0, 0.0};
+      dmma(d, a0, wa0);
+      dmma(d, a1, wa1);
+      g[blk(I, K)][0] = d[0];
+      g[blk(I, K)][1] = d[1];
+      c_to_a(d, lf[I][0], lf[I][1], lane);
+    }
+    // (c) trailing update
+#pragma unroll
+    for (int I = K + 1; I < NB; ++I)
+#pragma unroll
+      for (int J = K + 1; J <= I; ++J) {
+        dmma(g[blk(I, J)], -lf[I][0], lf[J][0]);
+        dmma(g[blk(I, J)], -lf[I][1], lf[J][1]);
+      }
+    // (d) forward substitution: y_K = W r_K; r_I -= L_IK y_K
+    store_c(T, r[K], lane);
+    __syncwarp();
+    {
+      const double b0 = T[t * 8 + q], b1 = T[(4 + t) * 8 + q];
+      double y[2] = {0.0, 0.0};
+      dmma(y, wa0, b0);
+      dmma(y, wa1, b1);
+      r[K][0] = y[0];
+      r[K][1] = y[1];
+    }
+    __syncwarp();
+    store_c(T, r[K], lane);
+    __syncwarp();
+    {
+      const double b0 = T[t * 8 + q], b1 = T[(4 + t) * 8 + q];
+#pragma unroll
+      for (int I = K + 1; I < NB; ++I) {
+        dmma(r[I], -lf[I][0], b0);
+        dmma(r[I], -lf[I][1], b1);
+      }
+    }
+    __syncwarp();
+  }
+
+  // ---------------------------------------------------------------- 4. backward
+#pragma unroll
+  for (int K = NB - 1; K >= 0; --K) {
+    double z[2] = {r[K][0], r[K][1]};
+#pragma unroll
+    for (int I = K + 1; I < NB; ++I) {
+      double a0, a1;
+      c_to_at(g[blk(I, K)], a0, a1, lane);  // L_IK^T
+      const double b0 = X[(I * 8 + t) * 8 + q], b1 = X[(I * 8 + 4 + t) * 8 + q];
+      dmma(z, -a0, b0);
+      dmma(z, -a1, b1);
+    }
+    store_c(T, z, lane);
+    __syncwarp();
+    const double* Wk = Wst + K * 64;
+    const double at0 = Wk[t * 8 + q], at1 = Wk[(4 + t) * 8 + q];  // W^T A-fragment
+    const double b0 = T[t * 8 + q], b1 = T[(4 + t) * 8 + q];
+    double x[2] = {0.0, 0.0};
+    dmma(x, at0, b0);
+    dmma(x, at1, b1);
+    __syncwarp();
+    X[(K * 8 + q) * 8 + 2 * t] = x[0];
+    X[(K * 8 + q) * 8 + 2 * t + 1] = x[1];
+    __syncwarp();
+  }
+
+  // ---------------------------------------------------------------- 5. output
+  bool finite = true;
+  for (int e = lane; e < NP * 8; e += 32) finite &= isfinite(X[e]);
+  ok = __all_sync(FULL, finite) && ok;
+  if (p.status && lane == 0) p.status[boff] = ok ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
+  const float nanf_ = __int_as_float(0x7fc00000);
+  for (int e = lane; e < p.n * p.C; e += 32) {
+    const int k = e / p.C, c = e % p.C;
+    double xr, xi;
+    if (MODE == MODE_SYMREAL) {
+      const int H8 = f.H8;
+      if ((p.n & 1) && k == h) {
+        xr = X[(2 * H8) * 8 + 2 * c];
+        xi = X[(2 * H8) * 8 + 2 * c + 1];
+      } else {
+        const bool hi = k >= h;
+        const int pp = hi ? p.n - 1 - k : k;
+        const double aa = X[pp * 8 + 2 * c], bb = X[pp * 8 + 2 * c + 1];
+        const double cc = X[(H8 + pp) * 8 + 2 * c], dd = X[(H8 + pp) * 8 + 2 * c + 1];
+        if (!hi) {
+          xr = (aa - dd) * M_SQRT1_2;
+          xi = (bb + cc) * M_SQRT1_2;
+        } else {
+          xr = (aa + dd) * M_SQRT1_2;
+          xi = (bb - cc) * M_SQRT1_2;
+        }
+      }
+    } else {
+      xr = X[k * 8 + 2 * c];
+      xi = X[k * 8 + 2 * c + 1];
+    }
+    p.layers[((size_t)k * p.C + c) * plane + boff] = ok ? make_float2((float)xr, (float)xi) : make_float2(nanf_, nanf_);
+  }
+}
+
+template <int NB, int MODE, int ODD>
+int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
+  const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hw : 0;
+  const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hw : 0;
+  const size_t smem = sizeof(double) * ((size_t)py_words + (size_t)WARPS * (px_words + 128 + NB * 64 + NB * 64));
+  if (smem > 220 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
+  auto kern = k1_fast_kernel<NB, MODE, ODD>;
+  FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)((p.Whp + WARPS - 1) / WARPS), (unsigned)p.nrows);
+  kern<<<grid, WARPS * 32, smem, st>>>(p, f);
+  FDL_LAUNCH_CHECK("k1_fast_kernel");
+  return FDL_OK;
+}
+
+template <int MODE, int ODD>
+int dispatch_nb(int NB, const SolveParams& p, const FastParams& f, cudaStream_t st) {
+  switch (NB) {
+    case 1: return launch_fast<1, MODE, ODD>(p, f, st);
+    case 2: return launch_fast<2, MODE, ODD>(p, f, st);
+    case 3: return launch_fast<3, MODE, ODD>(p, f, st);
+    case 4: return launch_fast<4, MODE, ODD>(p, f, st);
+    case 5: return launch_fast<5, MODE, ODD>(p, f, st);
+    case 6: return launch_fast<6, MODE, ODD>(p, f, st);
+    case 7: return launch_fast<7, MODE, ODD>(p, f, st);
+    case 8: return launch_fast<8, MODE, ODD>(p, f, st);
+    default: return fail(FDL_ERR_UNSUPPORTED, "NB");
+  }
+}
+
+// ---------------------------------------------------------------- self test
+__global__ void selftest_dmma_kernel(const double* A, const double* B, double* C) {
+  // C (8x8) = A (8x8) B (8x8) through two k4 steps, all layouts as documented
+  const int lane = threadIdx.x, q = lane >> 2, t = lane & 3;
+  double c[2] = {0.0, 0.0};
+  dmma(c, A[q * 8 + t], B[t * 8 + q]);
+  dmma(c, A[q * 8 + 4 + t], B[(4 + t) * 8 + q]);
+  C[q * 8 + 2 * t] = c[0];
+  C[q * 8 + 2 * t + 1] = c[1];
+  // and the shuffle converters: C-frag -> A-frag / transposed A-frag
+  double a0, a1, b0, b1;
+  c_to_a(c, a0, a1, lane);
+  c_to_at(c, b0, b1, lane);
+  C[64 + q * 8 + t] = a0;
+  C[64 + q * 8 + 4 + t] = a1;
+  C[128 + q * 8 + t] = b0;      // = C[t][q]
+  C[128 + q * 8 + 4 + t] = b1;  // = C[4+t][q]
+}
+
+}  // namespace
+
+int selftest_dmma(cudaStream_t st, double* max_err) {
+  double hA[64], hB[64], ref[64], out[192];
+  for (int e = 0; e < 64; ++e) {
+    hA[e] = 0.25 * (e % 7) - 0.5 + 0.01 * e;
+    hB[e] = 0.125 * (e % 5) + 0.003 * e - 0.2;
+  }
+  for (int r = 0; r < 8; ++r)
+    for (int c = 0; c < 8; ++c) {
+      double s = 0;
+      for (int k = 0; k < 8; ++k) s += hA[r * 8 + k] * hB[k * 8 + c];
+      ref[r * 8 + c] = s;
+    }
+  double* d;
+  FDL_CUDA_CHECK(cudaMalloc(&d, sizeof(double) * (64 + 64 + 192)));
+  FDL_CUDA_CHECK(cudaMemcpyAsync(d, hA, sizeof(hA), cudaMemcpyHostToDevice, st));
+  FDL_CUDA_CHECK(cudaMemcpyAsync(d + 64, hB, sizeof(hB), cudaMemcpyHostToDevice, st));
+  selftest_dmma_kernel<<<1, 32, 0, st>>>(d, d + 64, d + 128);
+  FDL_CUDA_CHECK(cudaMemcpyAsync(out, d + 128, sizeof(out), cudaMemcpyDeviceToHost, st));
+  FDL_CUDA_CHECK(cudaStreamSynchronize(st));
+  cudaFree(d);
+  double err = 0;
+  for (int r = 0; r < 8; ++r)
+    for (int c = 0; c < 8; ++c) {
+      err = fmax(err, fabs(out[r * 8 + c] - ref[r * 8 + c]));
+      err = fmax(err, fabs(out[64 + r * 8 + c] - ref[r * 8 + c]));
+      err = fmax(err, fabs(out[128 + r * 8 + c] - ref[c * 8 + r]));
+    }
+  *max_err = err;
+  return FDL_OK;
+}
+
+int k1_fast_launch(const SolveParams& p, cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (p.mode == MODE_COMPLEX) return FDL_OK;
+  if (p.C * 2 > 8) return FDL_OK;
+  int NB;
+  FastParams f{};
+  if (p.mode == MODE_SYMREAL) {
+    const int h = p.n / 2;
+    f.H8 = ((h + 7) / 8) * 8;
+    NB = 2 * f.H8 / 8 + (p.n & 1);
+    f.hw = h + (p.n & 1);
+    if (f.hw == 0) return FDL_OK;
+    // distinct u / v values (uploaded with the parameter block by the caller)
+    if (!p.fast_u_idx) return FDL_OK;
+    f.u_idx = p.fast_u_idx;
+    f.v_idx = p.fast_v_idx;
+    f.u_val = p.fast_u_val;
+    f.v_val = p.fast_v_val;
+    f.nu = p.fast_nu;
+    f.nv = p.fast_nv;
+  } else {
+    NB = (p.n + 7) / 8;
+  }
+  if (NB < 1 || NB > 8) return FDL_OK;
+  *handled = true;
+  if (p.mode == MODE_SYMREAL)
+    return (p.n & 1) ? dispatch_nb<MODE_SYMREAL, 1>(NB, p, f, st) : dispatch_nb<MODE_SYMREAL, 0>(NB, p, f, st);
+  return dispatch_nb<MODE_REALA, 0>(NB, p, f, st);
+}
+
+}  // namespace fdl

@@ -1,0 +1,180 @@
+// K3: batched render spectra (render.py:190-207, 238-245; lfmodel.py:101-122).
+//
+//   out[v, c, ky, kx] = sum_k L[k, c, ky, kx] * py_vk[ky] * px_vk[kx] * psi_v(t_vk wx, t_vk wy)
+//
+// The per-axis factors (phase exp(2 pi i P w) with cosine Nyquist lines, and
+// the separable bilinear aperture indices/fractions) depend on one axis only,
+// so a pre-pass evaluates them once per (view, layer, row|column) in float64
+// and stores them as float32 (`AxisFactor`); the hot kernel then does, per
+// (view, bin, layer), one complex product of the two axis phases, an optional
+// 2x2 bilinear gather from the float32 table and the complex MAC over
+// channels, all in float32 (>= 83 dB).
+#include "common.cuh"
+#include "k3_render.cuh"
+
+namespace fdl {
+
+namespace {
+
+__global__ void render_factors_kernel(RenderParams p) {
+  const int vk = blockIdx.x;  // v * n + k
+  const int v = vk / p.n;
+  const double P_u = p.pu[vk], P_v = p.pv[vk];
+  const int ai = p.view_ap ? p.view_ap[v] : -1;
+  const double t = (ai >= 0) ? p.t[vk] : 0.0;
+  const bool even_w = (p.Wp % 2) == 0, even_h = (p.Hp % 2) == 0;
+  AxisFactor* PX = p.px + (size_t)vk * p.Whp;
+  AxisFactor* PY = p.py + (size_t)vk * p.Hp;
+  int bad_x = 0, bad_y = 0;
+  for (int kx = threadIdx.x; kx < p.Whp; kx += blockDim.x) {
+    const double ox = omega_x_label(kx, p.Wp);
+    cd ph = axis_phase(P_u, ox, even_w && kx == p.Wp / 2);
+    AxisFactor f;
+    f.re = (float)ph.re;
+    f.im = (float)ph.im;
+    f.frac = 0.f;
+    f.idx = 0;
+    if (ai >= 0) {
+      const DevAperture& ap = p.aps[ai];
+      int i0;
+      double fr;
+      bool ok = axis_lookup(t * ox, ap.xi0_x, ap.step_x, ap.cols, i0, fr);
+      f.idx = ok ? i0 : -1;
+      f.frac = (float)fr;
+      bad_x += ok ? 0 : 1;
+    }
+    PX[kx] = f;
+  }
+  for (int ky = threadIdx.x; ky < p.Hp; ky += blockDim.x) {
+    const double oy = omega_y_label(ky, p.Hp);
+    cd ph = axis_phase(P_v, oy, even_h && ky == p.Hp / 2);
+    AxisFactor f;
+    f.re = (float)ph.re;
+    f.im = (float)ph.im;
+    f.frac = 0.f;
+    f.idx = 0;
+    if (ai >= 0) {
+      const DevAperture& ap = p.aps[ai];
+      int i0;
+      double fr;
+      bool ok = axis_lookup(t * oy, ap.xi0_y, ap.step_y, ap.rows, i0, fr);
+      f.idx = ok ? i0 : -1;
+      f.frac = (float)fr;
+      bad_y += ok ? 0 : 1;
+    }
+    PY[ky] = f;
+  }
+  if (ai >= 0 && p.oob) {
+    // lfmodel.py:118-121: n_oob = bad_rows * cols + ok_rows * bad_cols
+    __shared__ int sx, sy;
+    if (threadIdx.x == 0) {
+      sx = 0;
+      sy = 0;
+    }
+    __syncthreads();
+    atomicAdd(&sx, bad_x);
+    atomicAdd(&sy, bad_y);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long n_oob = (long long)sy * p.Whp + (long long)(p.Hp - sy) * sx;
+      if (n_oob) atomicAdd(reinterpret_cast<unsigned long long*>(p.oob + v), (unsigned long long)n_oob);
+    }
+  }
+}
+
+template <int C, int VB>
+__global__ void __launch_bounds__(256) render_sum_kernel(RenderParams p) {
+  const long long Q = (long long)p.Hp * p.Whp;
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int v0 = blockIdx.y * VB;
+  if (q >= Q) return;
+  const int ky = (int)(q / p.Whp), kx = (int)(q % p.Whp);
+  float2 acc[VB][C];
+#pragma unroll
+  for (int b = 0; b < VB; ++b)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[b][c] = make_float2(0.f, 0.f);
+  int apv[VB];
+#pragma unroll
+  for (int b = 0; b < VB; ++b) apv[b] = (v0 + b < p.V && p.view_ap) ? p.view_ap[v0 + b] : -1;
+
+  for (int k = 0; k < p.n; ++k) {
+    float2 L[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) L[c] = __ldg(p.layers + ((size_t)k * C + c) * Q + q);
+#pragma unroll
+    for (int b = 0; b < VB; ++b) {
+      const int v = v0 + b;
+      if (v >= p.V) break;
+      const size_t vk = (size_t)v * p.n + k;
+      const AxisFactor fx = p.px[vk * p.Whp + kx];
+      const AxisFactor fy = p.py[vk * p.Hp + ky];
+      float wr = fy.re * fx.re - fy.im * fx.im;
+      float wi = fy.re * fx.im + fy.im * fx.re;
+      if (apv[b] >= 0) {
+        const RenderTable& tb = p.tables[apv[b]];
+        if (fx.idx < 0 || fy.idx < 0) {
+          wr = 0.f;
+          wi = 0.f;
+        } else {
+          const size_t r0 = (size_t)fy.idx * tb.cols + fx.idx, r1 = r0 + tb.cols;
+          const float gx = fx.frac, gy = fy.frac;
+          // separable passes of lfmodel.py:115-116: rows first, then columns
+          float top = __ldg(tb.re + r0) * (1.f - gy) + __ldg(tb.re + r1) * gy;
+          float bot = __ldg(tb.re + r0 + 1) * (1.f - gy) + __ldg(tb.re + r1 + 1) * gy;
+          float sr = top * (1.f - gx) + bot * gx;
+          if (tb.im) {
+            float ti = __ldg(tb.im + r0) * (1.f - gy) + __ldg(tb.im + r1) * gy;
+            float bi = __ldg(tb.im + r0 + 1) * (1.f - gy) + __ldg(tb.im + r1 + 1) * gy;
+            float si = ti * (1.f - gx) + bi * gx;
+            float nr = wr * sr - wi * si;
+            wi = wr * si + wi * sr;
+            wr = nr;
+          } else {
+            wr *= sr;
+            wi *= sr;
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        acc[b][c].x = fmaf(wr, L[c].x, fmaf(-wi, L[c].y, acc[b][c].x));
+        acc[b][c].y = fmaf(wr, L[c].y, fmaf(wi, L[c].x, acc[b][c].y));
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    const int v = v0 + b;
+    if (v >= p.V) break;
+#pragma unroll
+    for (int c = 0; c < C; ++c) p.out[((size_t)v * C + c) * Q + q] = acc[b][c];
+  }
+}
+
+template <int C>
+int launch_sum(const RenderParams& p, cudaStream_t st) {
+  constexpr int VB = 4;
+  const long long Q = (long long)p.Hp * p.Whp;
+  dim3 grid((unsigned)((Q + 255) / 256), (unsigned)((p.V + VB - 1) / VB));
+  render_sum_kernel<C, VB><<<grid, 256, 0, st>>>(p);
+  FDL_LAUNCH_CHECK("render_sum_kernel");
+  return FDL_OK;
+}
+
+}  // namespace
+
+int render_launch(const RenderParams& p, cudaStream_t st) {
+  if (p.V == 0) return FDL_OK;
+  render_factors_kernel<<<p.V * p.n, 256, 0, st>>>(p);
+  FDL_LAUNCH_CHECK("render_factors_kernel");
+  switch (p.C) {
+    case 1: return launch_sum<1>(p, st);
+    case 2: return launch_sum<2>(p, st);
+    case 3: return launch_sum<3>(p, st);
+    case 4: return launch_sum<4>(p, st);
+    default: return fail(FDL_ERR_UNSUPPORTED, "render supports 1..4 channels");
+  }
+}
+
+}  // namespace fdl

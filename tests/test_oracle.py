@@ -1,0 +1,129 @@
+"""Pin the CPU oracle (oracle/fdl_oracle.py) to the reference's own outputs.
+
+The golden fixtures were produced by the reference package itself
+(tests/golden/make_golden.py).  The oracle calls the same numpy/LAPACK
+routines on the same operands, so agreement is expected to ~1e-13.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_aperture, load_golden, rel_l2
+from oracle import fdl_oracle as O
+
+CONSTRUCT_CASES = ["c1_full", "c2_s24", "c3_s32", "lambertian_lam1e-6", "lambertian_default", "odd_grid_n5"]
+
+
+def oracle_construct(g):
+    m = len(g["u"])
+    pu, pv = np.outer(g["u"], g["d"]), np.outer(g["v"], g["d"])
+    ap = golden_aperture(g, "ap")
+    views_ap = None if ap is None else [(ap, float(g["s"][j]), 1.0) for j in range(m)]
+    lam = None if np.isnan(g["lam_in"]) else float(g["lam_in"])
+    pad = None if int(g["pad_in"]) < 0 else int(g["pad_in"])
+    return O.construct(g["views"], pu, pv, g["d"], lam=lam, pad=pad, views_ap=views_ap)
+
+
+@pytest.mark.parametrize("name", CONSTRUCT_CASES)
+def test_oracle_construct_matches_reference(name):
+    g = load_golden(name)
+    out = oracle_construct(g)
+    assert out["pad"] == int(g["pad"])
+    assert out["lam"] == pytest.approx(float(g["lam"]), rel=1e-13)
+    assert rel_l2(out["layers"], g["layers"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", CONSTRUCT_CASES)
+def test_oracle_render_matches_reference(name):
+    g = load_golden(name)
+    n, C, hp, whp = g["layers"].shape
+    pad = int(g["pad"])
+    h, w = g["views"].shape[1:3]
+    for (u, v), ref in zip(g["render_uv"], g["renders"]):
+        img, _ = O.render(g["layers"], g["d"], hp, hp and (w + 2 * pad), pad, h, w, u=u, v=v)
+        assert np.max(np.abs(img - ref)) < 1e-12
+
+
+def test_oracle_c4_bins_match_reference():
+    g = load_golden("c4_s16_bins")
+    pad = int(g["pad"])
+    b_all, hp, wp = O.view_spectra(g["views"], pad)
+    whp = wp // 2 + 1
+    lam = O.default_lam(np.sum(np.abs(b_all) ** 2, axis=(1, 2)), len(g["u"]))
+    assert lam == pytest.approx(float(g["lam"]), rel=1e-13)
+    q = g["bins"]
+    pu, pv = np.outer(g["u"], g["d"]), np.outer(g["v"], g["d"])
+    px, py = O.axis_phases(pu, pv, wp, hp)
+    ox, oy = O.omega_axes(wp, hp)
+    kx, ky = q % whp, q // whp
+    A = O.system_block(px, py, kx, ky, g["d"], [(None, 0.0, 1.0)] * len(g["u"]), ox, oy)
+    reg = (ox[kx] ** 2 + oy[ky] ** 2)[:, None] ** 2 * g["d"][None, :] ** 4 + O.DEFAULT_EPS
+    x = O.normal_solve(A, b_all[q], reg, lam)
+    assert rel_l2(x, g["x"]) < 1e-12
+
+
+def test_oracle_render_c5_matches_reference():
+    g = load_golden("render_c5_small")
+    n, C, hp, whp = g["layers"].shape
+    wp = 40
+    ap = golden_aperture(g, "ap")
+    for i in range(len(g["u"])):
+        img, st = O.render(g["layers"], g["d"], hp, wp, 0, hp, wp, u=g["u"][i], v=g["v"][i], s=g["s"][i],
+                           f=g["f"][i], ap=ap)
+        assert np.max(np.abs(img - g["renders"][i])) < 1e-12
+        assert st["layer_ops"] == int(g["layer_ops"][i])
+        assert st["oob_lookups"] == int(g["oob"][i])
+    assert int(g["oob"][1]) > 0  # the wide request really exercises OOB
+
+
+def test_oracle_render_apertures_match_reference():
+    g = load_golden("render_apertures")
+    n, C, hp, whp = g["layers"].shape
+    wp, pad = 15, 1
+    poly, sq = golden_aperture(g, "poly"), golden_aperture(g, "sq")
+    assert np.iscomplexobj(poly[0]) and not np.iscomplexobj(sq[0])
+    specs = [(poly, False, True), (sq, True, True), (poly, False, False)]
+    for i, (ap, lin, crop) in enumerate(specs):
+        img, _ = O.render(g["layers"], g["d"], hp, wp, pad, hp - 2, wp - 2, u=g["req_u"][i], v=g["req_v"][i],
+                          s=g["req_s"][i], f=g["req_f"][i], ap=ap, gamma_linear=lin, crop=crop)
+        assert np.max(np.abs(img - g[f"render{i}"])) < 1e-12
+
+
+def test_oracle_relaxed_matches_reference():
+    g = load_golden("relaxed_n5")
+    out = O.construct(g["views"], g["pu"], g["pv"], g["d"], lam=1e-3)
+    assert rel_l2(out["layers"], g["layers"]) < 1e-12
+    h, w = g["views"].shape[1:3]
+    stack = O.render_with_shifts(out["layers"], g["pu"], g["pv"], out["hp"], out["wp"], out["pad"], h, w)
+    assert np.max(np.abs(stack - g["stack"])) < 1e-12
+
+
+@pytest.mark.parametrize("shape,params", [("disk", {"diameter": 8.0}), ("disk", {"diameter": 1.0}),
+                                          ("square", {"side": 0.5})])
+def test_oracle_aperture_tables_match_golden(shape, params):
+    g = load_golden("c3_s32") if params.get("diameter") == 8.0 else (
+        load_golden("render_c5_small") if shape == "disk" else load_golden("render_apertures"))
+    key = "sq" if shape == "square" else "ap"
+    tab, xx, xy = O.aperture_table(shape, **params)
+    assert np.array_equal(tab, g[f"{key}_table"])
+    assert np.array_equal(xx, g[f"{key}_xi_x"]) and np.array_equal(xy, g[f"{key}_xi_y"])
+
+
+def test_oracle_known_answers():
+    # test_construct.py:31-35: single-row phase e^{i pi/4}
+    px, py = O.axis_phases(np.array([[0.5]]), np.array([[0.0]]), 8, 8)
+    assert px[0, 0, 2] == pytest.approx(np.exp(1j * np.pi / 4), abs=1e-12)
+    # test_construct.py:61-68: scalar solves 2.0 and 0.5
+    x = O.normal_solve(np.array([[[2.0 + 0j]]]), np.array([[[4.0 + 0j]]]), np.array([[0.0]]), 0.0)
+    assert x[0, 0, 0] == pytest.approx(2.0, abs=1e-12)
+    x = O.normal_solve(np.array([[[1.0 + 0j]]]), np.array([[[1.0 + 0j]]]), np.array([[1.0]]), 1.0)
+    assert x[0, 0, 0] == pytest.approx(0.5, abs=1e-12)
+    # test_render.py:39-42: square sinc(0.5) = 2/pi
+    sq = O.aperture_table("square", pad_factor=8, side=1.0)
+    val, _ = O.aperture_eval(sq, 0.5, 0.0)
+    assert abs(val - 2 / np.pi) < 1e-3
+    # min-norm fallback of test_construct.py:98-105
+    A = np.ones((1, 3, 2), dtype=complex)
+    b = np.full((1, 3, 1), 2.0, dtype=complex)
+    x = O.normal_solve(A, b, np.full((1, 2), 1e-18), 1e-12)
+    assert abs(x[0, 0, 0] - x[0, 1, 0]) < 1e-6
