@@ -1,0 +1,394 @@
+"""Benchmark of the FDL construction + rendering hot paths (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = one construction of the FDL from the config's synthetic views
+(K0 pad + cuFFT R2C + sum|b|^2, default lambda, K1 per-bin fp64 solve, K2
+symmetrisation) followed by rendering every requested view (K3 + K4 C2R/crop).
+Default workload: config 2 (BASELINE.json configs[1]: 9x9 views, 512x512 RGB,
+30 layers; 81 input + 81 half-step renders).  Inputs are resident in HBM when
+the timed region starts; the views (255 MB) and layers exceed L2 (126 MB), so
+no explicit flush is needed.  `value` is construction throughput in
+frequency-layers per second (Q n / t); the render throughput is reported as
+`render.value` (views/s).  `e2e` times the same step through the public API
+(construct_fdl / render_many) from pinned host buffers with the host<->device
+copies inside the timed region.
+
+Multi-GPU (torchrun): every rank runs the same workload on its own replica
+(`scaling: weak`); the frequency-slab sharded construction lives in
+paper_1901_06919_b200/dist.py and is benchmarked with --sharded.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FP64_PEAK_TFLOPS = 36.88  # DMMA m8n8k4 measured on this pool's B200 (profiles/r01_fp64_pipes.txt)
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--size", type=int, default=None, help="override image size (testing)")
+    ap.add_argument("--batch", type=int, default=64, help="render views per K3 launch")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=24)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- workloads
+def canonical_flops_per_bin(cfg: str, m: int, n: int, C: int) -> float:
+    """SURVEY.md §8(d) algorithmic fp64 flops per bin of K1."""
+    if cfg == "c3":
+        return 4 * m * n * C + m * n * (n + 1) + n ** 3 / 3 + 4 * n * n * C
+    return 8 * m * n * C + 8 * m * n + (4.0 / 3.0) * n ** 3 + 8 * n * n * C
+
+
+def make_workload(cfg, size, device):
+    from harness.synth import make_case
+    if cfg == "c3":
+        from harness.focal import make_focal_case
+        return make_focal_case(size, device=device)
+    return make_case(cfg, size, device=device)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        os.remove(self.path)
+        if not rows:
+            return None
+        sm = [r[0] for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in rows), "samples": len(rows),
+                "reasons": reasons}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, device):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_06919_b200 as fdl
+    from paper_1901_06919_b200 import construct as K
+    import importlib
+    R = importlib.import_module("paper_1901_06919_b200.render")
+
+    case = make_workload(args.config, args.size, device)
+    views = case.views  # (m, H, W, C) float32 on the device
+    m, H, W, C = views.shape
+    d = case.d
+    n = len(d)
+    u, v = case.u, case.v
+    wide = case.aperture is not None
+    ap = fdl.aperture_spectrum(case.aperture["shape"], diameter=case.aperture["diameter"]) if wide else None
+    vs_meta = fdl.ViewSet(images=np.zeros((m, 1, 1, C), np.float32), u=u, v=v, s=case.s,
+                          apertures=[ap] * m if wide else None)
+    pu, pv = np.outer(u, d), np.outer(v, d)
+    pad = K.default_pad_margin(pu, pv)
+    Hp, Wp = H + 2 * pad, W + 2 * pad
+    Q = Hp * (Wp // 2 + 1)
+    rc = case.render_coords
+    reqs = [fdl.RenderRequest(u=float(a), v=float(b), f=0.0) for a, b in rc]
+    V = len(reqs)
+    stream = torch.cuda.current_stream()
+
+    def construct_step(ev=None):
+        spectra, sumsq = K.views_to_spectra(views, pad)
+        lam = K.lambda_from_sumsq(sumsq.cpu().numpy(), Q, m)
+        if ev is not None:
+            ev[0].record(stream)
+        layers, nbad, path = K.solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, lam, K.DEFAULT_EPS,
+                                          views=vs_meta, u=None if wide else u, v=None if wide else v)
+        if ev is not None:
+            ev[1].record(stream)
+        K.symmetrize(layers, Hp, Wp)
+        return fdl.FdlModel(disparities=d, layers=layers, grid=fdl.FrequencyGrid(Wp, Hp), width=W, height=H,
+                            pad_margin=pad), path
+
+    def render_step(model):
+        return R.render_many_device(model, reqs, batch=args.batch)
+
+    for _ in range(args.warmup):
+        model, path = construct_step()
+        render_step(model)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(device.index if device.index is not None else 0)
+    sampler.start()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for s in range(args.steps):
+        e = evs[s]
+        e[0].record(stream)
+        model, path = construct_step(ev=(e[3], e[4]))
+        e[1].record(stream)
+        render_step(model)
+        e[2].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    t_con = np.array([e[0].elapsed_time(e[1]) for e in evs]) / 1e3
+    t_ren = np.array([e[1].elapsed_time(e[2]) for e in evs]) / 1e3
+    t_k1 = np.array([e[3].elapsed_time(e[4]) for e in evs]) / 1e3
+    tot = np.array([t_con.sum(), t_ren.sum(), t_k1.sum()])
+    if world > 1:
+        tt = torch.tensor(tot, device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot = tt.cpu().numpy()
+    t_con_mean, t_ren_mean, t_k1_mean = tot / args.steps
+
+    # parity spot check on the last step (cheap): no NaN, layers finite
+    assert torch.isfinite(torch.view_as_real(model.layers_device())).all().item(), "non-finite layers"
+
+    F_bin = canonical_flops_per_bin(args.config, m, n, C)
+    achieved = F_bin * Q / t_k1_mean / 1e12
+    value = world * Q * n / t_con_mean
+    res = {
+        "metric": "FDL construction freq·layers/s and rendered views/s",
+        "value": value,
+        "unit": "freq·layers/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * (t_con_mean + t_ren_mean),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 solve / c64 I/O / f32 render",
+        "data": "synthetic (harness/synth.py seeded occluded layered scene, SURVEY.md §8(d))",
+        "config": {"workload": f"{args.config}: construct {m} views {H}x{W}x{C}, n={n} layers, pad {pad} "
+                               f"(Q={Q} bins), then render {V} views",
+                   "bins": Q, "views": m, "layers": n, "channels": C, "render_views": V,
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs (views, spectra, layers) exceed the 126 MB L2; no explicit flush",
+                   "k1_path": int(path)},
+        "render": {"value": world * V / t_ren_mean, "unit": "views/s", "ms": 1e3 * t_ren_mean},
+        "construct_ms": 1e3 * t_con_mean,
+        "k1_ms": 1e3 * t_k1_mean,
+        "roofline": {"bound": "tensor", "kernel": "k1_fast_kernel (fp64 DMMA)",
+                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "flops_per_bin": F_bin,
+                     "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r01_fp64_pipes.txt); "
+                                    "MEASURED_PEAKS.json has no fp64 entry"},
+        "clocks": clocks,
+        "gpu_launches": args.steps * (4 + 4 * math.ceil(V / args.batch)),
+    }
+    return res, case, (m, n, C, H, W, pad, Hp, Wp, Q, V)
+
+
+def run_e2e(args, case, dims, device):
+    """Same step through the public API from pinned host buffers."""
+    import torch
+
+    import paper_1901_06919_b200 as fdl
+    m, n, C, H, W, pad, Hp, Wp, Q, V = dims
+    host_views = torch.empty(tuple(case.views.shape), dtype=torch.float32, pin_memory=True)
+    host_views.copy_(case.views.cpu())
+    wide = case.aperture is not None
+    ap = fdl.aperture_spectrum(case.aperture["shape"], diameter=case.aperture["diameter"]) if wide else None
+    vs = fdl.ViewSet(images=host_views, u=case.u, v=case.v, s=case.s, apertures=[ap] * m if wide else None)
+    sh = fdl.ShiftParams.factored(case.u, case.v, case.d)
+    reqs = [fdl.RenderRequest(u=float(a), v=float(b), f=0.0) for a, b in case.render_coords]
+    out_host = torch.empty((n, C, Hp, Wp // 2 + 1), dtype=torch.complex64, pin_memory=True)
+
+    def step():
+        t0 = time.perf_counter()
+        model = fdl.construct_fdl(vs, sh)
+        out_host.copy_(model.layers_device(), non_blocking=True)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        imgs = fdl.render_many(model, reqs, batch=args.batch)
+        t2 = time.perf_counter()
+        return t1 - t0, t2 - t1, imgs
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    tc, tr = [], []
+    for _ in range(args.steps):
+        a, b, _ = step()
+        tc.append(a)
+        tr.append(b)
+    h2d = int(host_views.numel() * 4)
+    d2h = int(out_host.numel() * 8)
+    return {"value": Q * n / float(np.mean(tc)), "unit": "freq·layers/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h + V * H * W * C * 4,
+            "construct_ms": 1e3 * float(np.mean(tc)),
+            "render": {"value": V / float(np.mean(tr)), "unit": "views/s", "ms": 1e3 * float(np.mean(tr)),
+                       "d2h_bytes_per_step": V * H * W * C * 4}}
+
+
+# ----------------------------------------------------------------------------- CPU (oracle) arm
+def cpu_sample(args, case, dims, n_steps=1):
+    """The reference algorithm (oracle/fdl_oracle.py, pinned to the reference's
+    outputs) timed on the host: full view FFTs + lambda, the per-bin solves of a
+    bounded sample of mirrored frequency-row pairs (per-bin results are
+    chunk-independent, test_construct.py:196-204), extrapolated by bin count;
+    plus a few renders."""
+    from oracle import fdl_oracle as O
+    m, n, C, H, W, pad, Hp, Wp, Q, V = dims
+    views = case.views.cpu().numpy().astype(np.float64)
+    pu, pv = np.outer(case.u, case.d), np.outer(case.v, case.d)
+    views_ap = None
+    if case.aperture is not None:
+        tab = O.aperture_table(case.aperture["shape"], diameter=case.aperture["diameter"])
+        views_ap = [(tab, float(case.s[j]), 1.0) for j in range(m)]
+    whp = Wp // 2 + 1
+    nrow = max(2, min(args.cpu_sample_rows, Hp))
+    rows = np.unique(np.concatenate([np.arange(1, nrow // 2 + 1), Hp - np.arange(1, nrow // 2 + 1)]))
+    t_con, t_ren = [], []
+    c0 = time.process_time()
+    w0 = time.perf_counter()
+    for _ in range(n_steps):
+        t0 = time.perf_counter()
+        b_all, hp, wp = O.view_spectra(views, pad)
+        lam = O.default_lam(np.sum(np.abs(b_all) ** 2, axis=(1, 2)), m)
+        t1 = time.perf_counter()
+        b_rows = b_all.reshape(Hp, whp, m, C)[rows]
+        O.solve_rows(b_rows, rows, pu, pv, case.d, lam, Hp, Wp, views_ap=views_ap)
+        t2 = time.perf_counter()
+        t_con.append((t1 - t0) + (t2 - t1) * Hp / len(rows))
+        layers = np.zeros((n, C, Hp, whp), dtype=np.complex128)
+        r0 = time.perf_counter()
+        nr = 2
+        for (a, b) in case.render_coords[:nr]:
+            O.render(layers, case.d, Hp, Wp, pad, H, W, u=a, v=b)
+        t_ren.append((time.perf_counter() - r0) / nr)
+    cores = (time.process_time() - c0) / max(time.perf_counter() - w0, 1e-9)
+    sample = (f"full view FFTs + lambda, per-bin solves of {len(rows)} of {Hp} frequency rows "
+              f"(extrapolated x{Hp / len(rows):.1f}), {2} renders per step")
+    return float(np.mean(t_con)), float(np.mean(t_ren)), cores, sample
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU algorithm (oracle port) on the host cores."""
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    dev = "cpu"
+    case = make_workload(args.config, args.size, dev)
+    m, H, W, C = case.views.shape
+    n = len(case.d)
+    pu, pv = np.outer(case.u, case.d), np.outer(case.v, case.d)
+    pad = int(math.ceil(max(np.abs(pu).max(), np.abs(pv).max())))
+    Hp, Wp = H + 2 * pad, W + 2 * pad
+    Q = Hp * (Wp // 2 + 1)
+    V = len(case.render_coords)
+    dims = (m, n, C, H, W, pad, Hp, Wp, Q, V)
+    for _ in range(args.warmup and 1):
+        cpu_sample(args, case, dims)
+    t_con, t_ren, cores, sample = cpu_sample(args, case, dims, n_steps=args.steps)
+    value = Q * n / t_con
+    del torch
+    return {
+        "impl": "reference",
+        "metric": "FDL construction freq·layers/s and rendered views/s",
+        "value": value, "unit": "freq·layers/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * (t_con + V * t_ren), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: construct {m} views {H}x{W}x{C}, n={n} layers, pad {pad} "
+                               f"(Q={Q} bins), then render {V} views", "bins": Q, "render_views": V},
+        "render": {"value": 1.0 / t_ren, "unit": "views/s"},
+        "cpu_baseline": {"value": value, "unit": "freq·layers/s", "cores": round(cores, 2), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "freq·layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        res = run_reference(args)
+        if res is not None:
+            print(json.dumps(res))
+        return
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        print(json.dumps({"error": "no CUDA device"}))
+        sys.exit(1)
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    res, case, dims = run_ours(args, rank, world, device)
+    if not args.no_e2e:
+        res["e2e"] = run_e2e(args, case, dims, device)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t_con, t_ren, cores, sample = cpu_sample(args, case, dims)
+        res["cpu_baseline"] = {"value": dims[8] * dims[1] / t_con, "unit": "freq·layers/s", "cores": round(cores, 2),
+                               "kind": "port", "sample": sample, "render_views_per_s": 1.0 / t_ren}
+    if rank == 0:
+        print(json.dumps(res))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
