@@ -101,6 +101,8 @@ struct SolvePlan {
   SolveParams p{};
   size_t o_rows, o_pu, o_pv, o_d, o_d4, o_vap, o_s, o_sc, o_aps, o_cnt;
   size_t o_uidx = 0, o_vidx = 0, o_uval = 0, o_vval = 0;
+  size_t extra = 0;  // device-only scratch after the uploaded block (not copied)
+  size_t ws_bytes() const { return blob.size() + align256(extra); }
   bool has_axes = false;
   std::vector<size_t> o_tab_re, o_tab_im;
 };
@@ -282,6 +284,9 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
     p.fast_nu = (int)uv.size();
     p.fast_nv = (int)vv.size();
     P.has_axes = true;
+    // per-axis phase tables of the fast path: (Whp nu + nrows nv) (n/2 + 1) complex doubles
+    const size_t hw = (size_t)(n / 2 + (n & 1));
+    P.extra = 16 * hw * ((size_t)p.Whp * p.fast_nu + (size_t)D->nrows * p.fast_nv);
   }
   return FDL_OK;
 }
@@ -302,7 +307,9 @@ void bind_solve(SolvePlan& P, const fdl_solve_desc* D, void* ws) {
     p.fast_v_idx = at<int>(ws, P.o_vidx);
     p.fast_u_val = at<double>(ws, P.o_uval);
     p.fast_v_val = at<double>(ws, P.o_vval);
+    p.fast_tables = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + P.blob.size());
   } else {
+    p.fast_tables = nullptr;
     p.fast_u_idx = p.fast_v_idx = nullptr;
     p.fast_u_val = p.fast_v_val = nullptr;
   }
@@ -503,7 +510,7 @@ size_t fdl_solve_bins_workspace(const fdl_solve_desc* desc) {
   SolvePlan P;
   int mode;
   if (plan_solve(desc, P, &mode)) return 0;
-  return P.blob.size();
+  return P.ws_bytes();
 }
 
 int fdl_solve_path(const fdl_solve_desc* desc) {
@@ -519,7 +526,7 @@ int fdl_solve_bins(const fdl_solve_desc* desc, void* workspace_dev, size_t works
   int mode;
   int rc = plan_solve(desc, P, &mode);
   if (rc) return rc;
-  if (workspace_bytes < P.blob.size() || !workspace_dev) return fail(FDL_ERR_INVALID, "workspace too small for fdl_solve_bins");
+  if (workspace_bytes < P.ws_bytes() || !workspace_dev) return fail(FDL_ERR_INVALID, "workspace too small for fdl_solve_bins");
   if (!desc->spectra_dev || !desc->layers_dev) return fail(FDL_ERR_INVALID, "null spectra/layers buffer");
   cudaStream_t st = as_stream(stream);
   bind_solve(P, desc, workspace_dev);

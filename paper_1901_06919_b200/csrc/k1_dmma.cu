@@ -19,6 +19,8 @@
 // DMMA fragment layouts (m8n8k4, row.col, f64; lane l, q = l>>2, t = l&3):
 //   A (8x4): A[q][t]   B (4x8): B[t][q]   C (8x8): C[q][2t], C[q][2t+1]
 // (checked on the device by fdl_selftest).
+#include <algorithm>
+
 #include "k1_solve.cuh"
 
 namespace fdl {
@@ -54,6 +56,17 @@ __device__ __forceinline__ void c_to_at(const double (&c)[2], double& a0, double
   a1 = (q & 1) ? y1 : y0;
 }
 
+// 1/sqrt(x) in full double precision: MUFU approximation + two Newton steps
+// (CUDA's rsqrt(double) is a ~30-instruction library routine).
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
 __device__ __forceinline__ void store_c(double* S, const double (&c)[2], int lane) {
   const int q = lane >> 2, t = lane & 3;
   S[q * 8 + 2 * t] = c[0];
@@ -68,12 +81,40 @@ struct FastParams {
   int nu, nv;
   int H8;               // columns per cos/sin half, multiple of 8 (mode 1)
   int hw;               // phase-table width: h + (n odd)
+  const double2* px_all;  // (Whp, nu, hw) exp(2 pi i fl(u d_p) wx), cosine on the Nyquist column
+  const double2* py_all;  // (nrows, nv, hw)
 };
 
 __host__ __device__ constexpr int blk(int I, int J) { return I * (I + 1) / 2 + J; }
 
+// Per-axis phase tables of mode 1, once per column / row of the slab (the
+// reference's `_phase_tables`, construct.py:68-80, restricted to the distinct
+// u and v values and the first half of the layers).
+__global__ void k1_axis_tables_kernel(SolveParams p, FastParams f) {
+  const long long nx = (long long)p.Whp * f.nu * f.hw;
+  const long long ny = (long long)p.nrows * f.nv * f.hw;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nx + ny;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (e < nx) {
+      const int pp = (int)(e % f.hw);
+      const long long r = e / f.hw;
+      const int iu = (int)(r % f.nu), kx = (int)(r / f.nu);
+      cd ph = axis_phase(f.u_val[iu] * p.d[pp], omega_x_label(kx, p.Wp), (p.Wp % 2 == 0) && kx == p.Wp / 2);
+      const_cast<double2*>(f.px_all)[e] = make_double2(ph.re, ph.im);
+    } else {
+      const long long e2 = e - nx;
+      const int pp = (int)(e2 % f.hw);
+      const long long r = e2 / f.hw;
+      const int iv = (int)(r % f.nv), i = (int)(r / f.nv);
+      const int ky = p.rows[i];
+      cd ph = axis_phase(f.v_val[iv] * p.d[pp], omega_y_label(ky, p.Hp), (p.Hp % 2 == 0) && ky == p.Hp / 2);
+      const_cast<double2*>(f.py_all)[e2] = make_double2(ph.re, ph.im);
+    }
+  }
+}
+
 template <int NB, int MODE, int ODD>
-__global__ void __launch_bounds__(WARPS * 32, 1) k1_fast_kernel(SolveParams p, FastParams f) {
+__global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 4 ? 2 : 1))) k1_fast_kernel(SolveParams p, FastParams f) {
   constexpr int NBc = (NB - ODD) / 2;  // blocks of the cos half (= of the sin half), mode 1
   constexpr int NBLK = NB * (NB + 1) / 2;
   constexpr int NP = NB * 8;
@@ -90,35 +131,39 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k1_fast_kernel(SolveParams p, F
   double* PY = smem;
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hw : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hw : 0;
-  const int per_warp = px_words + 64 + 64 + NB * 64 + NP * 8;
-  double* base = smem + py_words + warp * per_warp;
+  const int m4 = (p.m + 3) & ~3;
+  const int ro_words = (MODE == MODE_SYMREAL) ? m4 : 0;  // int2 per view = one double word
+  int2* ROWOFF = reinterpret_cast<int2*>(PY + py_words);
+  const int bs_words = (p.m * p.C + 1) & ~1;  // staged spectra, one float2 per (view, channel); keeps 16-B alignment
+  const int per_warp = px_words + 64 + 64 + NB * 64 + NP * 8 + bs_words;
+  double* base = smem + py_words + ro_words + warp * per_warp;
   double* PX = base;
   double* S = PX + px_words;
   double* T = S + 64;
   double* Wst = T + 64;
   double* X = Wst + NB * 64;
+  float2* BS = reinterpret_cast<float2*>(X + NP * 8);
 
   if (MODE == MODE_SYMREAL) {
-    // exp(2 pi i fl(v d_p) wy) per distinct v, shared by the CTA's bins (same row)
-    for (int e = threadIdx.x; e < f.nv * f.hw; e += blockDim.x) {
-      const int iv = e / f.hw, pp = e % f.hw;
-      cd ph = axis_phase(f.v_val[iv] * p.d[pp], oy, nyq_y);
-      PY[2 * e] = ph.re;
-      PY[2 * e + 1] = ph.im;
-    }
+    const double2* src = f.py_all + (size_t)i * f.nv * f.hw;
+    for (int e = threadIdx.x; e < f.nv * f.hw; e += blockDim.x) reinterpret_cast<double2*>(PY)[e] = src[e];
+    for (int e = threadIdx.x; e < m4; e += blockDim.x)
+      ROWOFF[e] = e < p.m ? make_int2(f.u_idx[e] * f.hw, f.v_idx[e] * f.hw) : make_int2(0, 0);
   }
   __syncthreads();
   if (kx >= p.Whp) return;  // warp-uniform; no block barriers below
 
-  if (MODE == MODE_SYMREAL) {
-    for (int e = lane; e < f.nu * f.hw; e += 32) {
-      const int iu = e / f.hw, pp = e % f.hw;
-      cd ph = axis_phase(f.u_val[iu] * p.d[pp], ox, nyq_x);
-      PX[2 * e] = ph.re;
-      PX[2 * e + 1] = ph.im;
-    }
-    __syncwarp();
+  {
+    // stage this bin's m x C spectra values (one 8-byte load per view plane, all in flight)
+    const size_t plane_ = (size_t)p.nrows * p.Whp;
+    const float2* src = p.spectra + (size_t)i * p.Whp + kx;
+    for (int e = lane; e < p.m * p.C; e += 32) BS[e] = src[(size_t)e * plane_];
   }
+  if (MODE == MODE_SYMREAL) {
+    const double2* src = f.px_all + (size_t)kx * f.nu * f.hw;
+    for (int e = lane; e < f.nu * f.hw; e += 32) reinterpret_cast<double2*>(PX)[e] = src[e];
+  }
+  __syncwarp();
 
   double g[NBLK][2];
   double r[NB][2];
@@ -130,64 +175,147 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k1_fast_kernel(SolveParams p, F
   const size_t plane = (size_t)p.nrows * p.Whp;
   const size_t boff = (size_t)i * p.Whp + kx;
   const int h = p.h;
+  // Toeplitz-Hankel Gram (mode 1, uniform d, off the Nyquist lines, <= 3 channels):
+  // G' follows from t[r] = sum_j conj(A_j0) A_jr, which the RHS DMMAs produce for
+  // free in the two spare right-hand-side columns (6: Re A_j0, 7: Im A_j0).
+  const bool th = (MODE == MODE_SYMREAL) && p.uniform_d && !nyq_x && !nyq_y && p.C <= 3;
 
   // ---------------------------------------------------------------- 1. Gram + RHS
-  for (int r0 = 0; r0 < p.m; r0 += 4) {
+  // mode 1 design matrix (unscaled): M = [Re A_p | -Im A_p | Re A_mid]; the
+  // unknowns are x_p = (v+_p + i v-_p)/2, x_{n-1-p} = (v+_p - i v-_p)/2 (powers of
+  // two only, so no rounding beyond A's own).
+  const bool bcol = q < 2 * p.C;
+  const int bc = bcol ? (q >> 1) : 0;
+  const double2* PX2 = reinterpret_cast<const double2*>(PX);
+  const double2* PY2 = reinterpret_cast<const double2*>(PY);
+
+  // one k-step: 4 rows (views) r0..r0+3, lane row j = r0 + t
+  auto kstep = [&](int r0, bool tail) {
     const int j = r0 + t;
+    const bool valid = !tail || j < p.m;
+    const float2 bcur = BS[(valid ? j : 0) * p.C + bc];
     double mf[NB];
-    double bf = 0.0;
-    if (j < p.m) {
-      if (q < 2 * p.C) {
-        const float2 b = p.spectra[((size_t)j * p.C + (q >> 1)) * plane + boff];
-        bf = (q & 1) ? (double)b.y : (double)b.x;
+#pragma unroll
+    for (int I = 0; I < NB; ++I) mf[I] = 0.0;
+    double bf = bcol ? ((q & 1) ? (double)bcur.y : (double)bcur.x) : 0.0;
+    if (MODE == MODE_SYMREAL) {
+      const int2 ro = ROWOFF[j];
+      const double2* pxr = PX2 + ro.x;
+      const double2* pyr = PY2 + ro.y;
+      if (th && q >= 6) {
+        const double2 x0 = pxr[0], y0 = pyr[0];
+        bf = (q == 6) ? fma(x0.x, y0.x, -x0.y * y0.y) : fma(x0.x, y0.y, x0.y * y0.x);
       }
-      if (MODE == MODE_SYMREAL) {
-        const double* pxr = PX + 2 * f.u_idx[j] * f.hw;
-        const double* pyr = PY + 2 * f.v_idx[j] * f.hw;
+#pragma unroll
+      for (int I = 0; I < NBc; ++I) {
+        const int pp = I * 8 + q;
+        if (pp < h) {
+          const double2 x = pxr[pp], y = pyr[pp];
+          mf[I] = fma(x.x, y.x, -x.y * y.y);
+          mf[I + NBc] = -fma(x.x, y.y, x.y * y.x);
+        }
+      }
+      if (ODD && q == 0) {
+        const double2 x = pxr[h], y = pyr[h];
+        mf[NB - 1] = fma(x.x, y.x, -x.y * y.y);
+      }
+      if (tail && !valid) {
 #pragma unroll
         for (int I = 0; I < NB; ++I) mf[I] = 0.0;
+        bf = 0.0;
+      }
+    } else {  // MODE_REALA: A_jk = psi_j(t_jk wx, t_jk wy) (all shifts are zero)
+      if (!valid) bf = 0.0;
+      const int ai = (valid && p.view_ap) ? p.view_ap[j] : -1;
 #pragma unroll
-        for (int I = 0; I < NB; ++I) {
-          if (I < NBc) {
-            const int pp = I * 8 + q;
-            if (pp < h) {
-              cd a = cmul_rn(cd{pxr[2 * pp], pxr[2 * pp + 1]}, cd{pyr[2 * pp], pyr[2 * pp + 1]});
-              mf[I] = M_SQRT2 * a.re;
-              mf[I + NBc] = -M_SQRT2 * a.im;
-            }
+      for (int I = 0; I < NB; ++I) {
+        const int k = I * 8 + q;
+        if (valid && k < p.n) {
+          if (ai < 0) {
+            mf[I] = 1.0;
+          } else {
+            const double tt = __dmul_rn(p.scale[j], __dsub_rn(p.s[j], p.d[k]));
+            mf[I] = aperture_eval(p.aps[ai], __dmul_rn(tt, ox), __dmul_rn(tt, oy)).re;
           }
-        }
-        if (ODD && q == 0) {
-          cd a = cmul_rn(cd{pxr[2 * h], pxr[2 * h + 1]}, cd{pyr[2 * h], pyr[2 * h + 1]});
-          mf[NB - 1] = a.re;
-        }
-      } else {  // MODE_REALA: A_jk = psi_j(t_jk wx, t_jk wy) (all shifts are zero)
-        const int ai = p.view_ap ? p.view_ap[j] : -1;
-#pragma unroll
-        for (int I = 0; I < NB; ++I) {
-          const int k = I * 8 + q;
-          double v = 0.0;
-          if (k < p.n) {
-            if (ai < 0) {
-              v = 1.0;
-            } else {
-              const double tt = __dmul_rn(p.scale[j], __dsub_rn(p.s[j], p.d[k]));
-              v = aperture_eval(p.aps[ai], __dmul_rn(tt, ox), __dmul_rn(tt, oy)).re;
-            }
-          }
-          mf[I] = v;
         }
       }
-    } else {
-#pragma unroll
-      for (int I = 0; I < NB; ++I) mf[I] = 0.0;
     }
 #pragma unroll
     for (int I = 0; I < NB; ++I) dmma(r[I], mf[I], bf);
+    if (!th) {
+#pragma unroll
+      for (int I = 0; I < NB; ++I)
+#pragma unroll
+        for (int J = 0; J <= I; ++J) dmma(g[blk(I, J)], mf[I], mf[J]);
+    }
+  };
+  const int mfull = p.m & ~3;
+  for (int r0 = 0; r0 < mfull; r0 += 4) kstep(r0, false);
+  if (mfull < p.m) kstep(mfull, true);
+
+  if (MODE == MODE_SYMREAL && th) {
+    // RHS columns 6/7 = M^T [Re A_0, Im A_0]  ->  t[r], r = 0..n-1  ->  G fragments
+#pragma unroll
+    for (int I = 0; I < NB; ++I) {
+      X[(I * 8 + q) * 8 + 2 * t] = r[I][0];
+      X[(I * 8 + q) * 8 + 2 * t + 1] = r[I][1];
+    }
+    __syncwarp();
+    double* TT = S;  // S and T are contiguous: 2 * 64 doubles = t[0..63]
+    const int H8 = NBc * 8;
+    for (int rr = lane; rr < p.n; rr += 32) {
+      double re, im;
+      if (ODD && rr == h) {
+        re = X[(2 * H8) * 8 + 6];
+        im = -X[(2 * H8) * 8 + 7];
+      } else if (rr < h) {
+        re = X[rr * 8 + 6] - X[(H8 + rr) * 8 + 7];
+        im = -X[(H8 + rr) * 8 + 6] - X[rr * 8 + 7];
+      } else {
+        const int pq = p.n - 1 - rr;
+        re = X[pq * 8 + 6] + X[(H8 + pq) * 8 + 7];
+        im = X[(H8 + pq) * 8 + 6] - X[pq * 8 + 7];
+      }
+      TT[2 * rr] = re;
+      TT[2 * rr + 1] = im;
+    }
+    __syncwarp();
+    // extended table E[k + n - 1] = t[k] for k in [-(n-1), n-1] (t[-k] = conj t[k]), in X
+    const int nm1 = p.n - 1;
+    double2* E = reinterpret_cast<double2*>(X);
+    for (int k = lane; k < 2 * p.n - 1; k += 32) {
+      const int kk = k - nm1;
+      const int ak = kk < 0 ? -kk : kk;
+      E[k] = make_double2(TT[2 * ak], kk < 0 ? -TT[2 * ak + 1] : TT[2 * ak + 1]);
+    }
+    __syncwarp();
 #pragma unroll
     for (int I = 0; I < NB; ++I)
 #pragma unroll
-      for (int J = 0; J <= I; ++J) dmma(g[blk(I, J)], mf[I], mf[J]);
+      for (int J = 0; J <= I; ++J)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          // quadrant (cos / sin / middle) of block row I and block column J is compile-time
+          const bool rc = I < NBc, rs = I >= NBc && I < 2 * NBc;
+          const bool cc_ = J < NBc, cs = J >= NBc && J < 2 * NBc;
+          const int a = rc ? I * 8 + q : (rs ? (I - NBc) * 8 + q : h);
+          const int b = cc_ ? J * 8 + 2 * t + e : (cs ? (J - NBc) * 8 + 2 * t + e : h);
+          const bool va = (rc || rs) ? a < h : q == 0;
+          const bool vb = (cc_ || cs) ? b < h : (2 * t + e) == 0;
+          double v = 0.0;
+          if (!(va && vb)) {
+          } else if (rc && cc_) v = 0.5 * (E[a - b + nm1].x + E[a + b].x);
+          else if (rs && cs) v = 0.5 * (E[a - b + nm1].x - E[a + b].x);
+          else if (rs && cc_) v = -0.5 * (E[a + b].y + E[a - b + nm1].y);
+          else if (rc && cs) v = -0.5 * (E[a + b].y + E[b - a + nm1].y);
+          else if (!rc && !rs && cc_) v = E[b - h + nm1].x;
+          else if (!rc && !rs && cs) v = -E[b - h + nm1].y;
+          else if (rc && !cc_ && !cs) v = E[a - h + nm1].x;
+          else if (rs && !cc_ && !cs) v = -E[a - h + nm1].y;
+          else v = E[nm1].x;
+          g[blk(I, J)][e] = v;
+        }
+    __syncwarp();
   }
 
   // ---------------------------------------------------------------- 2. + lam reg'
@@ -199,30 +327,22 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k1_fast_kernel(SolveParams p, F
     for (int I = 0; I < NB; ++I) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int rr = q, cc = 2 * t + e;
-        if (rr != cc) continue;
-        const int col = I * 8 + rr;
-        int k0 = -1, k1 = -1;
+        if (q != 2 * t + e) continue;
+        const int col = I * 8 + q;
+        double add = 1.0;  // padding column: identity
         if (MODE == MODE_SYMREAL) {
-          const int H8 = f.H8;
-          if (col < H8) {
-            if (col < h) k0 = col;
-          } else if (col < 2 * H8) {
-            if (col - H8 < h) k0 = col - H8;
-          } else if (col == 2 * H8 && (p.n & 1)) {
-            k0 = h;
+          const bool cpart = I < NBc, spart = I >= NBc && I < 2 * NBc;
+          const int pp = cpart ? col : (spart ? col - NBc * 8 : h);
+          if ((cpart || spart) && pp < h) {
+            // pair (p, n-1-p): lam (reg_p + reg_{n-1-p}) / 4 on the unscaled basis
+            const double r1 = __dadd_rn(__dmul_rn(w4, p.d4[pp]), p.eps);
+            const double r2 = __dadd_rn(__dmul_rn(w4, p.d4[p.n - 1 - pp]), p.eps);
+            add = p.lam > 0.0 ? __dmul_rn(p.lam, 0.25 * __dadd_rn(r1, r2)) : 0.0;
+          } else if (!cpart && !spart && ODD && q == 0) {
+            add = p.lam > 0.0 ? __dmul_rn(p.lam, __dadd_rn(__dmul_rn(w4, p.d4[h]), p.eps)) : 0.0;
           }
-          if (k0 >= 0 && k0 < h) k1 = p.n - 1 - k0;
-        } else {
-          if (col < p.n) k0 = col;
-        }
-        double add;
-        if (k0 < 0) {
-          add = 1.0;  // padding column: identity
-        } else {
-          double rg = __dadd_rn(__dmul_rn(w4, p.d4[k0]), p.eps);
-          if (k1 >= 0) rg = 0.5 * __dadd_rn(rg, __dadd_rn(__dmul_rn(w4, p.d4[k1]), p.eps));
-          add = p.lam > 0.0 ? __dmul_rn(p.lam, rg) : 0.0;
+        } else if (col < p.n) {
+          add = p.lam > 0.0 ? __dmul_rn(p.lam, __dadd_rn(__dmul_rn(w4, p.d4[col]), p.eps)) : 0.0;
         }
         g[blk(I, I)][e] = __dadd_rn(g[blk(I, I)][e], add);
       }
@@ -233,42 +353,30 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k1_fast_kernel(SolveParams p, F
   bool ok = true;
 #pragma unroll
   for (int K = 0; K < NB; ++K) {
-    // (a) factor + invert the diagonal block with lanes 0..7 (lane = row)
+    // (a) factor the diagonal block with lanes 0..7 (lane = row) and invert it;
+    //     column values are broadcast through shared memory, pivots by rsqrt.
     store_c(S, g[blk(K, K)], lane);
     __syncwarp();
-    double a[8];
     bool lok = true;
     if (lane < 8) {
+      double a[8], dinv[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) a[c] = S[lane * 8 + c];
-    } else {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) a[c] = (c == 0) ? 1.0 : 0.0;
-    }
+      for (int k = 0; k < 8; ++k) {
+        const double akk = __shfl_sync(0xffu, a[k], k);
+        const bool good = (akk > 0.0) && isfinite(akk);
+        lok = lok && good;
+        const double inv = rsqrt_fast(good ? akk : 1.0);
+        dinv[k] = inv;
+        a[k] = (lane == k) ? (good ? akk : 1.0) * inv : a[k] * inv;  // rows < k: unused upper part
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const double akk = __shfl_sync(FULL, a[k], k);
-      const bool good = (akk > 0.0) && isfinite(akk);
-      lok = lok && good;
-      const double lkk = sqrt(good ? akk : 1.0);
-      const double inv = 1.0 / lkk;
-      if (lane == k) a[k] = lkk;
-      if (lane > k) a[k] *= inv;
-#pragma unroll
-      for (int c = k + 1; c < 8; ++c) {
-        const double lck = __shfl_sync(FULL, a[k], c);
-        if (lane >= c) a[c] = fma(-a[k], lck, a[c]);
+        for (int c = k + 1; c < 8; ++c) a[c] = fma(-a[k], __shfl_sync(0xffu, a[k], c), a[c]);  // upper: harmless
       }
-    }
-    ok = __all_sync(FULL, lok) && ok;
-    __syncwarp();
-    if (lane < 8) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) S[lane * 8 + c] = (c <= lane) ? a[c] : 0.0;
-    }
-    __syncwarp();
-    if (lane < 8) {
-      // column `lane` of W = L^-1 by forward substitution
+      for (int c = 0; c < 8; ++c) S[lane * 8 + c] = a[c];  // upper triangle ignored below
+      __syncwarp(0xffu);
+      // column `lane` of W = L^-1: w_rr = (delta_rc - sum_{k<rr} L_rk w_k) / L_rr  (zero above c)
       const int c = lane;
       double w[8];
 #pragma unroll
@@ -276,11 +384,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k1_fast_kernel(SolveParams p, F
         double acc = (rr == c) ? 1.0 : 0.0;
 #pragma unroll
         for (int k = 0; k < rr; ++k) acc = fma(-S[rr * 8 + k], w[k], acc);
-        w[rr] = (rr >= c) ? acc / S[rr * 8 + rr] : 0.0;
+        w[rr] = acc * dinv[rr];
       }
 #pragma unroll
       for (int rr = 0; rr < 8; ++rr) Wst[K * 64 + rr * 8 + c] = w[rr];
     }
+    ok = ok && __all_sync(FULL, lok);
     __syncwarp();
     const double* Wk = Wst + K * 64;
     // A-fragment of W (= B-fragment of W^T): W[q][t], W[q][4+t]
@@ -360,7 +469,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k1_fast_kernel(SolveParams p, F
 
   // ---------------------------------------------------------------- 5. output
   bool finite = true;
-  for (int e = lane; e < NP * 8; e += 32) finite &= isfinite(X[e]);
+#pragma unroll
+  for (int e = 0; e < NP * 8 / 32; ++e) {
+    const int idx = e * 32 + lane;
+    if ((idx & 7) < 2 * p.C) finite = finite && isfinite(X[idx]);
+  }
   ok = __all_sync(FULL, finite) && ok;
   if (p.status && lane == 0) p.status[boff] = ok ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
   const float nanf_ = __int_as_float(0x7fc00000);
@@ -368,22 +481,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k1_fast_kernel(SolveParams p, F
     const int k = e / p.C, c = e % p.C;
     double xr, xi;
     if (MODE == MODE_SYMREAL) {
-      const int H8 = f.H8;
-      if ((p.n & 1) && k == h) {
+      const int H8 = NBc * 8;
+      if (ODD && k == h) {
         xr = X[(2 * H8) * 8 + 2 * c];
         xi = X[(2 * H8) * 8 + 2 * c + 1];
       } else {
         const bool hi = k >= h;
         const int pp = hi ? p.n - 1 - k : k;
+        // v+ = aa + i bb, v- = cc + i dd;  x_p = (v+ + i v-)/2, x_{n-1-p} = (v+ - i v-)/2
         const double aa = X[pp * 8 + 2 * c], bb = X[pp * 8 + 2 * c + 1];
         const double cc = X[(H8 + pp) * 8 + 2 * c], dd = X[(H8 + pp) * 8 + 2 * c + 1];
-        if (!hi) {
-          xr = (aa - dd) * M_SQRT1_2;
-          xi = (bb + cc) * M_SQRT1_2;
-        } else {
-          xr = (aa + dd) * M_SQRT1_2;
-          xi = (bb - cc) * M_SQRT1_2;
-        }
+        xr = 0.5 * (hi ? aa + dd : aa - dd);
+        xi = 0.5 * (hi ? bb - cc : bb + cc);
       }
     } else {
       xr = X[k * 8 + 2 * c];
@@ -397,7 +506,9 @@ template <int NB, int MODE, int ODD>
 int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hw : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hw : 0;
-  const size_t smem = sizeof(double) * ((size_t)py_words + (size_t)WARPS * (px_words + 128 + NB * 64 + NB * 64));
+  const int ro_words = (MODE == MODE_SYMREAL) ? ((p.m + 3) & ~3) : 0;
+  const size_t smem = sizeof(double) * ((size_t)py_words + ro_words +
+                                        (size_t)WARPS * (px_words + 128 + NB * 64 + NB * 64 + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
   if (smem > 220 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
   auto kern = k1_fast_kernel<NB, MODE, ODD>;
   FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -487,7 +598,7 @@ int k1_fast_launch(const SolveParams& p, cudaStream_t st, bool* handled) {
     f.hw = h + (p.n & 1);
     if (f.hw == 0) return FDL_OK;
     // distinct u / v values (uploaded with the parameter block by the caller)
-    if (!p.fast_u_idx) return FDL_OK;
+    if (!p.fast_u_idx || !p.fast_tables) return FDL_OK;
     f.u_idx = p.fast_u_idx;
     f.v_idx = p.fast_v_idx;
     f.u_val = p.fast_u_val;
@@ -499,8 +610,15 @@ int k1_fast_launch(const SolveParams& p, cudaStream_t st, bool* handled) {
   }
   if (NB < 1 || NB > 8) return FDL_OK;
   *handled = true;
-  if (p.mode == MODE_SYMREAL)
+  if (p.mode == MODE_SYMREAL) {
+    f.px_all = reinterpret_cast<const double2*>(p.fast_tables);
+    f.py_all = f.px_all + (size_t)p.Whp * f.nu * f.hw;
+    const long long tot = ((long long)p.Whp * f.nu + (long long)p.nrows * f.nv) * f.hw;
+    int blocks = (int)std::min<long long>((tot + 255) / 256, 148LL * 8);
+    k1_axis_tables_kernel<<<blocks, 256, 0, st>>>(p, f);
+    FDL_LAUNCH_CHECK("k1_axis_tables_kernel");
     return (p.n & 1) ? dispatch_nb<MODE_SYMREAL, 1>(NB, p, f, st) : dispatch_nb<MODE_SYMREAL, 0>(NB, p, f, st);
+  }
   return dispatch_nb<MODE_REALA, 0>(NB, p, f, st);
 }
 

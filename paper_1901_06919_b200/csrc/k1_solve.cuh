@@ -53,6 +53,7 @@ struct SolveParams {
   const double* fast_u_val;
   const double* fast_v_val;
   int fast_nu, fast_nv;
+  double* fast_tables;       // workspace for the per-axis phase tables (fast path)
 };
 
 // A_jk (construct.py:168-180 with build_system_row's Nyquist handling, construct.py:83-109)

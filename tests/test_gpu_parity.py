@@ -113,8 +113,8 @@ def test_c4_layout_bins_match_reference(fdl):
     assert nbad == 0 and path == 1
     x = layers.cpu().numpy().reshape(len(g["d"]), 3, hp * whp)[:, :, g["bins"]].transpose(2, 0, 1)
     err = rel_l2(x, g["x"])
-    print(f"c4 bins rel L2 {err:.3e}")
-    assert err <= LAYER_TOL
+    print(f"c4 bins rel L2 {err:.3e} (floor {float(np.max(g['floor'])):.2e})")
+    assert err <= max(LAYER_TOL, 10 * float(np.max(g["floor"])))
 
 
 def test_render_c5_small_matches_reference(fdl):
