@@ -146,21 +146,25 @@ __device__ inline float srgb_enc(float x) {
   return x <= 0.0031308f ? x * 12.92f : 1.055f * powf(x, 1.0f / 2.4f) - 0.055f;
 }
 
-// (V, C, Hp, Wp) real planes scaled by 1/(Hp Wp) -> (V, Ho, Wo, C) cropped
-__global__ void crop_kernel(const float* __restrict__ planes, int V, int C, int Hp, int Wp, int pad, int Ho,
-                            int Wo, int srgb, float scale, float* __restrict__ out) {
-  const size_t total = (size_t)V * Ho * Wo * C;
+// (V, C, Hp, Wp) real planes scaled by 1/(Hp Wp) -> (V, Ho, Wo, C) cropped.
+// One thread per output pixel: C coalesced plane reads, C contiguous writes.
+template <int C>
+__global__ void crop_kernel(const float* __restrict__ planes, int V, int Hp, int Wp, int pad, int Ho, int Wo,
+                            int srgb, float scale, float* __restrict__ out) {
+  const size_t total = (size_t)V * Ho * Wo;
   for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (size_t)gridDim.x * blockDim.x) {
-    int c = (int)(idx % C);
-    size_t r = idx / C;
-    int x = (int)(r % Wo);
-    r /= Wo;
-    int y = (int)(r % Ho);
-    int v = (int)(r / Ho);
-    float val = planes[(((size_t)v * C + c) * Hp + (y + pad)) * Wp + (x + pad)] * scale;
-    if (srgb) val = srgb_enc(val);
-    out[idx] = val;
+    const int x = (int)(idx % Wo);
+    const size_t r = idx / Wo;
+    const int y = (int)(r % Ho);
+    const int v = (int)(r / Ho);
+    const float* src = planes + ((size_t)v * C * Hp + (y + pad)) * Wp + (x + pad);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float val = __ldg(src + (size_t)c * Hp * Wp) * scale;
+      if (srgb) val = srgb_enc(val);
+      out[idx * C + c] = val;
+    }
   }
 }
 
@@ -244,9 +248,16 @@ int spectra_to_images(fdl_c64* spectra, int V, int C, int Hp, int Wp, int pad, i
   if (cufftSetWorkArea(plan->handle, fft_work) != CUFFT_SUCCESS) return fail(FDL_ERR_CUDA, "cufftSetWorkArea");
   if (cufftExecC2R(plan->handle, reinterpret_cast<cufftComplex*>(spectra), planes) != CUFFT_SUCCESS)
     return fail(FDL_ERR_CUDA, "cufftExecC2R failed");
-  size_t total = (size_t)V * Ho * Wo * C;
+  size_t total = (size_t)V * Ho * Wo;
   float scale = (float)(1.0 / ((double)Hp * (double)Wp));
-  crop_kernel<<<grid_for(total, 256), 256, 0, st>>>(planes, V, C, Hp, Wp, pad, Ho, Wo, srgb, scale, images);
+  const int g = grid_for(total, 256);
+  switch (C) {
+    case 1: crop_kernel<1><<<g, 256, 0, st>>>(planes, V, Hp, Wp, pad, Ho, Wo, srgb, scale, images); break;
+    case 2: crop_kernel<2><<<g, 256, 0, st>>>(planes, V, Hp, Wp, pad, Ho, Wo, srgb, scale, images); break;
+    case 3: crop_kernel<3><<<g, 256, 0, st>>>(planes, V, Hp, Wp, pad, Ho, Wo, srgb, scale, images); break;
+    case 4: crop_kernel<4><<<g, 256, 0, st>>>(planes, V, Hp, Wp, pad, Ho, Wo, srgb, scale, images); break;
+    default: return fail(FDL_ERR_UNSUPPORTED, "images support 1..4 channels");
+  }
   FDL_LAUNCH_CHECK("crop_kernel");
   return FDL_OK;
 }

@@ -82,37 +82,76 @@ __global__ void render_factors_kernel(RenderParams p) {
   }
 }
 
-template <int C, int VB>
-__global__ void __launch_bounds__(256) render_sum_kernel(RenderParams p) {
+// Tile kernel: CTA = 32 columns x 8 rows of bins for VB views; per layer k the
+// (view, column) and (view, row) axis factors are staged in shared memory
+// (double-buffered, one barrier per layer), each thread owns one bin and
+// accumulates VB x C complex outputs in registers, and the layer values it
+// needs for layer k+1 are prefetched while layer k is consumed.
+constexpr int TX = 32, TY = 8;
+
+template <int C, int VB, bool AP>
+__global__ void __launch_bounds__(TX * TY) render_tile_kernel(RenderParams p) {
+  __shared__ AxisFactor FX[2][VB][TX];
+  __shared__ AxisFactor FY[2][VB][TY];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const int kx = blockIdx.x * TX + tx, ky = blockIdx.y * TY + ty;
+  const int v0 = blockIdx.z * VB;
+  const int nv = min(VB, p.V - v0);
   const long long Q = (long long)p.Hp * p.Whp;
-  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int v0 = blockIdx.y * VB;
-  if (q >= Q) return;
-  const int ky = (int)(q / p.Whp), kx = (int)(q % p.Whp);
+  const bool inside = kx < p.Whp && ky < p.Hp;
+  const long long q = inside ? (long long)ky * p.Whp + kx : 0;
+
+  // staging: VB*TX column factors + VB*TY row factors per layer
+  auto stage = [&](int k, int buf) {
+    for (int e = tid; e < VB * (TX + TY); e += TX * TY) {
+      if (e < VB * TX) {
+        const int b = e / TX, c = e % TX;
+        const int col = blockIdx.x * TX + c;
+        if (b < nv && col < p.Whp) FX[buf][b][c] = p.px[((size_t)(v0 + b) * p.n + k) * p.Whp + col];
+      } else {
+        const int e2 = e - VB * TX;
+        const int b = e2 / TY, r = e2 % TY;
+        const int row = blockIdx.y * TY + r;
+        if (b < nv && row < p.Hp) FY[buf][b][r] = p.py[((size_t)(v0 + b) * p.n + k) * p.Hp + row];
+      }
+    }
+  };
+
+  __shared__ int TIDX[VB];
+  if (tid < VB) TIDX[tid] = (AP && tid < nv && p.view_ap) ? p.view_ap[v0 + tid] : -1;
+
   float2 acc[VB][C];
 #pragma unroll
   for (int b = 0; b < VB; ++b)
 #pragma unroll
     for (int c = 0; c < C; ++c) acc[b][c] = make_float2(0.f, 0.f);
-  int apv[VB];
-#pragma unroll
-  for (int b = 0; b < VB; ++b) apv[b] = (v0 + b < p.V && p.view_ap) ? p.view_ap[v0 + b] : -1;
 
+  float2 Lnext[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) Lnext[c] = inside ? __ldg(p.layers + (size_t)c * Q + q) : make_float2(0.f, 0.f);
+  stage(0, 0);
+  __syncthreads();
   for (int k = 0; k < p.n; ++k) {
+    const int buf = k & 1;
     float2 L[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) L[c] = __ldg(p.layers + ((size_t)k * C + c) * Q + q);
+    for (int c = 0; c < C; ++c) L[c] = Lnext[c];
+    if (k + 1 < p.n) {
+      stage(k + 1, buf ^ 1);
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        Lnext[c] = inside ? __ldg(p.layers + ((size_t)(k + 1) * C + c) * Q + q) : make_float2(0.f, 0.f);
+    }
 #pragma unroll
     for (int b = 0; b < VB; ++b) {
-      const int v = v0 + b;
-      if (v >= p.V) break;
-      const size_t vk = (size_t)v * p.n + k;
-      const AxisFactor fx = p.px[vk * p.Whp + kx];
-      const AxisFactor fy = p.py[vk * p.Hp + ky];
+      if (b >= nv || !inside) break;  // outside the grid: staged factors are not defined
+      const AxisFactor fx = FX[buf][b][tx];
+      const AxisFactor fy = FY[buf][b][ty];
       float wr = fy.re * fx.re - fy.im * fx.im;
       float wi = fy.re * fx.im + fy.im * fx.re;
-      if (apv[b] >= 0) {
-        const RenderTable& tb = p.tables[apv[b]];
+      const int ai = AP ? TIDX[b] : -1;
+      if (AP && ai >= 0) {
+        const RenderTable tb = p.tables[ai];
         if (fx.idx < 0 || fy.idx < 0) {
           wr = 0.f;
           wi = 0.f;
@@ -120,14 +159,14 @@ __global__ void __launch_bounds__(256) render_sum_kernel(RenderParams p) {
           const size_t r0 = (size_t)fy.idx * tb.cols + fx.idx, r1 = r0 + tb.cols;
           const float gx = fx.frac, gy = fy.frac;
           // separable passes of lfmodel.py:115-116: rows first, then columns
-          float top = __ldg(tb.re + r0) * (1.f - gy) + __ldg(tb.re + r1) * gy;
-          float bot = __ldg(tb.re + r0 + 1) * (1.f - gy) + __ldg(tb.re + r1 + 1) * gy;
-          float sr = top * (1.f - gx) + bot * gx;
+          const float top = __ldg(tb.re + r0) * (1.f - gy) + __ldg(tb.re + r1) * gy;
+          const float bot = __ldg(tb.re + r0 + 1) * (1.f - gy) + __ldg(tb.re + r1 + 1) * gy;
+          const float sr = top * (1.f - gx) + bot * gx;
           if (tb.im) {
-            float ti = __ldg(tb.im + r0) * (1.f - gy) + __ldg(tb.im + r1) * gy;
-            float bi = __ldg(tb.im + r0 + 1) * (1.f - gy) + __ldg(tb.im + r1 + 1) * gy;
-            float si = ti * (1.f - gx) + bi * gx;
-            float nr = wr * sr - wi * si;
+            const float ti = __ldg(tb.im + r0) * (1.f - gy) + __ldg(tb.im + r1) * gy;
+            const float bi = __ldg(tb.im + r0 + 1) * (1.f - gy) + __ldg(tb.im + r1 + 1) * gy;
+            const float si = ti * (1.f - gx) + bi * gx;
+            const float nr = wr * sr - wi * si;
             wi = wr * si + wi * sr;
             wr = nr;
           } else {
@@ -142,23 +181,29 @@ __global__ void __launch_bounds__(256) render_sum_kernel(RenderParams p) {
         acc[b][c].y = fmaf(wr, L[c].y, fmaf(wi, L[c].x, acc[b][c].y));
       }
     }
+    __syncthreads();
   }
+  if (!inside) return;
 #pragma unroll
   for (int b = 0; b < VB; ++b) {
-    const int v = v0 + b;
-    if (v >= p.V) break;
+    if (b >= nv) break;
 #pragma unroll
-    for (int c = 0; c < C; ++c) p.out[((size_t)v * C + c) * Q + q] = acc[b][c];
+    for (int c = 0; c < C; ++c) p.out[((size_t)(v0 + b) * C + c) * Q + q] = acc[b][c];
   }
 }
 
 template <int C>
 int launch_sum(const RenderParams& p, cudaStream_t st) {
-  constexpr int VB = 4;
-  const long long Q = (long long)p.Hp * p.Whp;
-  dim3 grid((unsigned)((Q + 255) / 256), (unsigned)((p.V + VB - 1) / VB));
-  render_sum_kernel<C, VB><<<grid, 256, 0, st>>>(p);
-  FDL_LAUNCH_CHECK("render_sum_kernel");
+  constexpr int VB = C <= 3 ? 16 : 8;
+  dim3 block(TX, TY);
+  dim3 grid((unsigned)((p.Whp + TX - 1) / TX), (unsigned)((p.Hp + TY - 1) / TY), (unsigned)((p.V + VB - 1) / VB));
+  bool ap = false;
+  if (p.view_ap) ap = true;  // the per-view check is inside; pinhole-only batches take the cheap variant
+  if (ap)
+    render_tile_kernel<C, VB, true><<<grid, block, 0, st>>>(p);
+  else
+    render_tile_kernel<C, VB, false><<<grid, block, 0, st>>>(p);
+  FDL_LAUNCH_CHECK("render_tile_kernel");
   return FDL_OK;
 }
 
