@@ -425,8 +425,9 @@ int plan_render(const fdl_render_desc* D, RenderPlan& P) {
 
 size_t render_ws_bytes(const RenderPlan& P) {
   const RenderParams& p = P.p;
-  return P.blob.size() + align256(sizeof(AxisFactor) * (size_t)p.V * p.n * p.Whp) +
-         align256(sizeof(AxisFactor) * (size_t)p.V * p.n * p.Hp);
+  const size_t ve = (size_t)((p.V + 1) & ~1);  // pinhole layout pairs views
+  return P.blob.size() + align256(sizeof(AxisFactor) * ve * p.n * p.Whp) +
+         align256(sizeof(AxisFactor) * ve * p.n * p.Hp);
 }
 
 void bind_render(RenderPlan& P, const fdl_render_desc* D, void* ws) {
@@ -459,7 +460,7 @@ void bind_render(RenderPlan& P, const fdl_render_desc* D, void* ws) {
   }
   char* base = reinterpret_cast<char*>(ws) + P.blob.size();
   p.px = reinterpret_cast<AxisFactor*>(base);
-  p.py = reinterpret_cast<AxisFactor*>(base + align256(sizeof(AxisFactor) * (size_t)p.V * p.n * p.Whp));
+  p.py = reinterpret_cast<AxisFactor*>(base + align256(sizeof(AxisFactor) * (size_t)((p.V + 1) & ~1) * p.n * p.Whp));
 }
 
 }  // namespace

@@ -25,6 +25,10 @@ __global__ void render_factors_kernel(RenderParams p) {
   const bool even_w = (p.Wp % 2) == 0, even_h = (p.Hp % 2) == 0;
   AxisFactor* PX = p.px + (size_t)vk * p.Whp;
   AxisFactor* PY = p.py + (size_t)vk * p.Hp;
+  // pinhole batches: view pairs interleaved, float2 phases: px2[(v/2, k, kx)][v&1]
+  const bool pin = p.view_ap == nullptr;
+  float2* PX2 = reinterpret_cast<float2*>(p.px) + (((size_t)(v >> 1) * p.n + (vk - v * p.n)) * p.Whp) * 2 + (v & 1);
+  float2* PY2 = reinterpret_cast<float2*>(p.py) + (((size_t)(v >> 1) * p.n + (vk - v * p.n)) * p.Hp) * 2 + (v & 1);
   int bad_x = 0, bad_y = 0;
   for (int kx = threadIdx.x; kx < p.Whp; kx += blockDim.x) {
     const double ox = omega_x_label(kx, p.Wp);
@@ -43,7 +47,10 @@ __global__ void render_factors_kernel(RenderParams p) {
       f.frac = (float)fr;
       bad_x += ok ? 0 : 1;
     }
-    PX[kx] = f;
+    if (pin)
+      PX2[2 * (size_t)kx] = make_float2(f.re, f.im);
+    else
+      PX[kx] = f;
   }
   for (int ky = threadIdx.x; ky < p.Hp; ky += blockDim.x) {
     const double oy = omega_y_label(ky, p.Hp);
@@ -62,7 +69,10 @@ __global__ void render_factors_kernel(RenderParams p) {
       f.frac = (float)fr;
       bad_y += ok ? 0 : 1;
     }
-    PY[ky] = f;
+    if (pin)
+      PY2[2 * (size_t)ky] = make_float2(f.re, f.im);
+    else
+      PY[ky] = f;
   }
   if (ai >= 0 && p.oob) {
     // lfmodel.py:118-121: n_oob = bad_rows * cols + ok_rows * bad_cols
@@ -89,10 +99,21 @@ __global__ void render_factors_kernel(RenderParams p) {
 // needs for layer k+1 are prefetched while layer k is consumed.
 constexpr int TX = 32, TY = 8;
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int src_size = valid ? 16 : 0;  // 0: zero-fill (weight 0)
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gsrc), "r"(src_size));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+constexpr int NSTAGE = 3;  // factor ring: layer k in use, k+1 and k+2 in flight
+
 template <int C, int VB, bool AP>
-__global__ void __launch_bounds__(TX * TY) render_tile_kernel(RenderParams p) {
-  __shared__ AxisFactor FX[2][VB][TX];
-  __shared__ AxisFactor FY[2][VB][TY];
+__global__ void __launch_bounds__(TX * TY, 2) render_tile_kernel(RenderParams p) {
+  __shared__ __align__(16) AxisFactor FX[NSTAGE][VB][TX];
+  __shared__ __align__(16) AxisFactor FY[NSTAGE][VB][TY];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
   const int kx = blockIdx.x * TX + tx, ky = blockIdx.y * TY + ty;
   const int v0 = blockIdx.z * VB;
@@ -101,24 +122,31 @@ __global__ void __launch_bounds__(TX * TY) render_tile_kernel(RenderParams p) {
   const bool inside = kx < p.Whp && ky < p.Hp;
   const long long q = inside ? (long long)ky * p.Whp + kx : 0;
 
-  // staging: VB*TX column factors + VB*TY row factors per layer
-  auto stage = [&](int k, int buf) {
+  // asynchronous staging of layer k's VB*TX column + VB*TY row factors; entries
+  // outside the grid / past the last view are zero-filled (weight 0), so the
+  // compute loop runs branch-free for every thread and view slot
+  auto stage = [&](int k) {
+    const int buf = k % NSTAGE;
     for (int e = tid; e < VB * (TX + TY); e += TX * TY) {
       if (e < VB * TX) {
         const int b = e / TX, c = e % TX;
         const int col = blockIdx.x * TX + c;
-        if (b < nv && col < p.Whp) FX[buf][b][c] = p.px[((size_t)(v0 + b) * p.n + k) * p.Whp + col];
+        const bool ok = b < nv && col < p.Whp;
+        cp_async16(&FX[buf][b][c], p.px + (ok ? ((size_t)(v0 + b) * p.n + k) * p.Whp + col : 0), ok);
       } else {
         const int e2 = e - VB * TX;
         const int b = e2 / TY, r = e2 % TY;
         const int row = blockIdx.y * TY + r;
-        if (b < nv && row < p.Hp) FY[buf][b][r] = p.py[((size_t)(v0 + b) * p.n + k) * p.Hp + row];
+        const bool ok = b < nv && row < p.Hp;
+        cp_async16(&FY[buf][b][r], p.py + (ok ? ((size_t)(v0 + b) * p.n + k) * p.Hp + row : 0), ok);
       }
     }
+    cp_async_commit();
   };
 
   __shared__ int TIDX[VB];
   if (tid < VB) TIDX[tid] = (AP && tid < nv && p.view_ap) ? p.view_ap[v0 + tid] : -1;
+  // (made visible by the first __syncthreads of the layer loop)
 
   float2 acc[VB][C];
 #pragma unroll
@@ -129,24 +157,33 @@ __global__ void __launch_bounds__(TX * TY) render_tile_kernel(RenderParams p) {
   float2 Lnext[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) Lnext[c] = inside ? __ldg(p.layers + (size_t)c * Q + q) : make_float2(0.f, 0.f);
-  stage(0, 0);
-  __syncthreads();
+  stage(0);
+  if (p.n > 1) stage(1);
   for (int k = 0; k < p.n; ++k) {
-    const int buf = k & 1;
+    const int buf = k % NSTAGE;
+    if (k + 2 < p.n) {
+      stage(k + 2);
+      cp_async_wait<2>();
+    } else if (k + 1 < p.n) {
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // layer k's factors visible to all threads
     float2 L[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) L[c] = Lnext[c];
     if (k + 1 < p.n) {
-      stage(k + 1, buf ^ 1);
 #pragma unroll
       for (int c = 0; c < C; ++c)
         Lnext[c] = inside ? __ldg(p.layers + ((size_t)(k + 1) * C + c) * Q + q) : make_float2(0.f, 0.f);
     }
+    const AxisFactor* fxp = &FX[buf][0][tx];
+    const AxisFactor* fyp = &FY[buf][0][ty];
 #pragma unroll
     for (int b = 0; b < VB; ++b) {
-      if (b >= nv || !inside) break;  // outside the grid: staged factors are not defined
-      const AxisFactor fx = FX[buf][b][tx];
-      const AxisFactor fy = FY[buf][b][ty];
+      const AxisFactor fx = fxp[b * TX];
+      const AxisFactor fy = fyp[b * TY];
       float wr = fy.re * fx.re - fy.im * fx.im;
       float wi = fy.re * fx.im + fy.im * fx.re;
       const int ai = AP ? TIDX[b] : -1;
@@ -181,9 +218,101 @@ __global__ void __launch_bounds__(TX * TY) render_tile_kernel(RenderParams p) {
         acc[b][c].y = fmaf(wr, L[c].y, fmaf(wi, L[c].x, acc[b][c].y));
       }
     }
-    __syncthreads();
+    __syncthreads();  // buffer k % NSTAGE is refilled by stage(k + 3)
   }
   if (!inside) return;
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    if (b >= nv) break;
+#pragma unroll
+    for (int c = 0; c < C; ++c) p.out[((size_t)(v0 + b) * C + c) * Q + q] = acc[b][c];
+  }
+}
+
+// Pinhole tile kernel (no aperture in the batch): factors are view-pair
+// interleaved float2 phases, so one 16-byte shared load serves two views and
+// each layer's staging is one 16-byte cp.async per thread.
+template <int C, int VB>
+__global__ void __launch_bounds__(TX * TY, 2) render_pin_kernel(RenderParams p) {
+  constexpr int NP = VB / 2;
+  __shared__ __align__(16) float4 FX2[NSTAGE][NP][TX];
+  __shared__ __align__(16) float4 FY2[NSTAGE][NP][TY];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const int kx = blockIdx.x * TX + tx, ky = blockIdx.y * TY + ty;
+  const int v0 = blockIdx.z * VB;
+  const int npairs = min(NP, (p.V - v0 + 1) / 2);
+  const long long Q = (long long)p.Hp * p.Whp;
+  const bool inside = kx < p.Whp && ky < p.Hp;
+  const long long q = inside ? (long long)ky * p.Whp + kx : 0;
+  const float4* PXG = reinterpret_cast<const float4*>(p.px);
+  const float4* PYG = reinterpret_cast<const float4*>(p.py);
+  const int pr0 = v0 / 2;
+
+  // staging of one layer: NP*TX column pairs (one 16-byte cp.async per thread)
+  // + NP*TY row pairs (threads < NP*TY); zero-filled outside the grid
+  static_assert(NP * TX <= TX * TY, "at most one column-factor copy per thread");
+  const int spr = tid / TX, sc = tid % TX;
+  const int scol = blockIdx.x * TX + sc;
+  const bool sxact = tid < NP * TX;
+  const bool sxok = sxact && spr < npairs && scol < p.Whp;
+  const float4* sx = PXG + (sxok ? (size_t)(pr0 + spr) * p.n * p.Whp + scol : 0);
+  const int ypr = tid / TY, yr = tid % TY;
+  const int srow = blockIdx.y * TY + yr;
+  const bool syact = tid < NP * TY;
+  const bool syok = syact && ypr < npairs && srow < p.Hp;
+  const float4* sy = PYG + (syok ? (size_t)(pr0 + ypr) * p.n * p.Hp + srow : 0);
+  auto stage = [&](int k) {
+    const int buf = k % NSTAGE;
+    if (sxact) cp_async16(&FX2[buf][spr][sc], sxok ? sx + (size_t)k * p.Whp : PXG, sxok);
+    if (syact) cp_async16(&FY2[buf][ypr][yr], syok ? sy + (size_t)k * p.Hp : PYG, syok);
+    cp_async_commit();
+  };
+
+  float2 acc[VB][C];
+#pragma unroll
+  for (int b = 0; b < VB; ++b)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[b][c] = make_float2(0.f, 0.f);
+  float2 Lnext[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) Lnext[c] = inside ? __ldg(p.layers + (size_t)c * Q + q) : make_float2(0.f, 0.f);
+  stage(0);
+  if (p.n > 1) stage(1);
+  const float2* lp = p.layers + q;  // + (k * C + c) * Q
+  for (int k = 0; k < p.n; ++k) {
+    const int buf = k % NSTAGE;
+    if (k + 1 < p.n) cp_async_wait<1>(); else cp_async_wait<0>();
+    __syncthreads();  // layer k's factors visible; everyone is done with layer k-1's buffer
+    if (k + 2 < p.n) stage(k + 2);  // refills the buffer of layer k-1
+    float2 L[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) L[c] = Lnext[c];
+    if (k + 1 < p.n) {
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        Lnext[c] = inside ? __ldg(lp + ((size_t)(k + 1) * C + c) * Q) : make_float2(0.f, 0.f);
+    }
+    const float4* fxp = &FX2[buf][0][tx];
+    const float4* fyp = &FY2[buf][0][ty];
+#pragma unroll
+    for (int pr = 0; pr < NP; ++pr) {
+      const float4 fx = fxp[pr * TX];
+      const float4 fy = fyp[pr * TY];
+      const float w0r = fy.x * fx.x - fy.y * fx.y, w0i = fy.x * fx.y + fy.y * fx.x;
+      const float w1r = fy.z * fx.z - fy.w * fx.w, w1i = fy.z * fx.w + fy.w * fx.z;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        float2& a0 = acc[2 * pr][c];
+        float2& a1 = acc[2 * pr + 1][c];
+        a0.x = fmaf(w0r, L[c].x, fmaf(-w0i, L[c].y, a0.x));
+        a0.y = fmaf(w0r, L[c].y, fmaf(w0i, L[c].x, a0.y));
+        a1.x = fmaf(w1r, L[c].x, fmaf(-w1i, L[c].y, a1.x));
+        a1.y = fmaf(w1r, L[c].y, fmaf(w1i, L[c].x, a1.y));
+      }
+    }
+  }
+  if (!inside) return;
+  const int nv = min(VB, p.V - v0);
 #pragma unroll
   for (int b = 0; b < VB; ++b) {
     if (b >= nv) break;
@@ -197,12 +326,10 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
   constexpr int VB = C <= 3 ? 16 : 8;
   dim3 block(TX, TY);
   dim3 grid((unsigned)((p.Whp + TX - 1) / TX), (unsigned)((p.Hp + TY - 1) / TY), (unsigned)((p.V + VB - 1) / VB));
-  bool ap = false;
-  if (p.view_ap) ap = true;  // the per-view check is inside; pinhole-only batches take the cheap variant
-  if (ap)
+  if (p.view_ap)  // some view of the batch has an aperture: the per-view check is inside
     render_tile_kernel<C, VB, true><<<grid, block, 0, st>>>(p);
   else
-    render_tile_kernel<C, VB, false><<<grid, block, 0, st>>>(p);
+    render_pin_kernel<C, VB><<<grid, block, 0, st>>>(p);
   FDL_LAUNCH_CHECK("render_tile_kernel");
   return FDL_OK;
 }
