@@ -39,6 +39,14 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 FP64_PEAK_TFLOPS = 36.88  # DMMA m8n8k4 measured on this pool's B200 (profiles/r01_fp64_pipes.txt)
+TRAFFIC_FILE = ROOT / "profiles" / "k1_traffic.json"  # dram bytes per K1 launch from `ncu --set full`
+
+
+def k1_traffic(cfg: str):
+    try:
+        return json.load(open(TRAFFIC_FILE)).get(cfg)
+    except Exception:
+        return None
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 
 
@@ -193,6 +201,7 @@ def run_ours(args, rank, world, device):
     torch.cuda.synchronize()
     sampler = ClockSampler(device.index if device.index is not None else 0)
     sampler.start()
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ isolates the step's launches
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     for s in range(args.steps):
         e = evs[s]
@@ -201,6 +210,7 @@ def run_ours(args, rank, world, device):
         e[1].record(stream)
         render_step(model)
         e[2].record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -248,7 +258,9 @@ def run_ours(args, rank, world, device):
         "k1_ms": 1e3 * t_k1_mean,
         "roofline": {"bound": "tensor", "kernel": "k1_fast_kernel (fp64 DMMA)",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "frac": achieved / FP64_PEAK_TFLOPS,
+                     "traffic": k1_traffic(args.config) if world == 1 else None,
+                     "algorithmic_bytes": 8 * C * (m + n) * q_k1,
                      "flops_per_bin": F_bin,
                      "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r01_fp64_pipes.txt); "
                                     "MEASURED_PEAKS.json has no fp64 entry"},
