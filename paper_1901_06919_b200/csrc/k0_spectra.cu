@@ -62,32 +62,63 @@ int get_plan(int h, int w, int batch, int type, Plan** out) {
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// views (m,H,W,C) -> padded planar (m,C,Hp,Wp)
-__global__ void pack_pad_kernel(const float* __restrict__ views, int m, int H, int W, int C, int pad,
+// views (m,H,W,C) -> padded planar (m,C,Hp,Wp).  One thread per (view, padded
+// row, 4 consecutive padded columns): reads the 4*C interleaved input floats,
+// writes one float4 per channel plane (Wp % 4 == 0) or 4 scalars.
+template <int C>
+__global__ void pack_pad_kernel(const float* __restrict__ views, int m, int H, int W, int pad,
                                 float* __restrict__ out) {
   const int Hp = H + 2 * pad, Wp = W + 2 * pad;
-  const size_t total = (size_t)m * C * Hp * Wp;
+  const int W4 = (Wp + 3) / 4;
+  const size_t total = (size_t)m * Hp * W4;
+  const bool vec = (Wp % 4) == 0;
   for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (size_t)gridDim.x * blockDim.x) {
-    int x = (int)(idx % Wp);
-    size_t r = idx / Wp;
-    int y = (int)(r % Hp);
-    r /= Hp;
-    int c = (int)(r % C);
-    int j = (int)(r / C);
-    int xs = x - pad, ys = y - pad;
-    float v = 0.f;
-    if (xs >= 0 && xs < W && ys >= 0 && ys < H) v = __ldg(views + (((size_t)j * H + ys) * W + xs) * C + c);
-    out[idx] = v;
+    const int x4 = (int)(idx % W4);
+    const size_t r = idx / W4;
+    const int y = (int)(r % Hp);
+    const int j = (int)(r / Hp);
+    const int ys = y - pad;
+    float v[4][C];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int xs = x4 * 4 + e - pad;
+      const bool in = ys >= 0 && ys < H && xs >= 0 && xs < W;
+      const float* src = views + (((size_t)j * H + (in ? ys : 0)) * W + (in ? xs : 0)) * C;
+#pragma unroll
+      for (int c = 0; c < C; ++c) v[e][c] = in ? __ldg(src + c) : 0.f;
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float* dst = out + (((size_t)j * C + c) * Hp + y) * Wp + x4 * 4;
+      if (vec) {
+        *reinterpret_cast<float4*>(dst) = make_float4(v[0][c], v[1][c], v[2][c], v[3][c]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (x4 * 4 + e < Wp) dst[e] = v[e][c];
+      }
+    }
   }
 }
 
-// one block per view: sum over (C, Hp, Whp) of |b|^2 in float64, fixed order
-__global__ void view_sumsq_kernel(const float2* __restrict__ spec, size_t per_view, double* __restrict__ out) {
-  const float2* p = spec + (size_t)blockIdx.x * per_view;
+template <int C>
+void launch_pack(const float* views, int m, int H, int W, int pad, float* out, int grid, cudaStream_t st) {
+  pack_pad_kernel<C><<<grid, 256, 0, st>>>(views, m, H, W, pad, out);
+}
+
+// sum over (C, Hp, Whp) of |b|^2 per view in float64, deterministic: SPLIT
+// blocks per view write partials, a second kernel adds them in a fixed order.
+constexpr int SUMSQ_SPLIT = 16;
+__global__ void view_sumsq_partial_kernel(const float2* __restrict__ spec, size_t per_view,
+                                          double* __restrict__ partial) {
+  const int view = blockIdx.x / SUMSQ_SPLIT, part = blockIdx.x % SUMSQ_SPLIT;
+  const size_t chunk = (per_view + SUMSQ_SPLIT - 1) / SUMSQ_SPLIT;
+  const size_t b0 = (size_t)part * chunk, b1 = min(per_view, b0 + chunk);
+  const float2* p = spec + (size_t)view * per_view;
   double acc = 0.0;
-  for (size_t i = threadIdx.x; i < per_view; i += blockDim.x) {
-    float2 b = p[i];
+  for (size_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+    const float2 b = p[i];
     acc += (double)b.x * b.x + (double)b.y * b.y;
   }
   __shared__ double red[32];
@@ -97,8 +128,16 @@ __global__ void view_sumsq_kernel(const float2* __restrict__ spec, size_t per_vi
   if (threadIdx.x < 32) {
     double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) out[blockIdx.x] = v;
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
   }
+}
+
+__global__ void view_sumsq_final_kernel(const double* __restrict__ partial, int m, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double s = 0.0;
+  for (int k = 0; k < SUMSQ_SPLIT; ++k) s += partial[(size_t)j * SUMSQ_SPLIT + k];
+  out[j] = s;
 }
 
 __global__ void gather_rows_kernel(const float2* __restrict__ src, int planes, int Hp, int Whp,
@@ -182,7 +221,8 @@ int views_to_spectra_ws(int m, int H, int W, int C, int pad, size_t* bytes) {
   Plan* plan;
   int rc = get_plan(Hp, Wp, m * C, 0, &plan);
   if (rc) return rc;
-  *bytes = align256((size_t)m * C * Hp * Wp * sizeof(float)) + align256(plan->work);
+  *bytes = align256((size_t)m * C * Hp * Wp * sizeof(float)) + align256(plan->work) +
+           align256(sizeof(double) * (size_t)m * SUMSQ_SPLIT);
   return FDL_OK;
 }
 
@@ -197,17 +237,26 @@ int views_to_spectra(const float* views, int m, int H, int W, int C, int pad, fd
   get_plan(Hp, Wp, m * C, 0, &plan);
   float* padded = reinterpret_cast<float*>(ws);
   void* fft_work = reinterpret_cast<char*>(ws) + align256((size_t)m * C * Hp * Wp * sizeof(float));
-  size_t total = (size_t)m * C * Hp * Wp;
-  pack_pad_kernel<<<grid_for(total, 256), 256, 0, st>>>(views, m, H, W, C, pad, padded);
+  const int g = grid_for((size_t)m * Hp * ((Wp + 3) / 4), 256);
+  switch (C) {
+    case 1: launch_pack<1>(views, m, H, W, pad, padded, g, st); break;
+    case 2: launch_pack<2>(views, m, H, W, pad, padded, g, st); break;
+    case 3: launch_pack<3>(views, m, H, W, pad, padded, g, st); break;
+    case 4: launch_pack<4>(views, m, H, W, pad, padded, g, st); break;
+    default: return fail(FDL_ERR_UNSUPPORTED, "views support 1..4 channels");
+  }
   FDL_LAUNCH_CHECK("pack_pad_kernel");
   if (cufftSetStream(plan->handle, st) != CUFFT_SUCCESS) return fail(FDL_ERR_CUDA, "cufftSetStream");
   if (cufftSetWorkArea(plan->handle, fft_work) != CUFFT_SUCCESS) return fail(FDL_ERR_CUDA, "cufftSetWorkArea");
   if (cufftExecR2C(plan->handle, padded, reinterpret_cast<cufftComplex*>(spectra)) != CUFFT_SUCCESS)
     return fail(FDL_ERR_CUDA, "cufftExecR2C failed");
   if (view_sumsq) {
-    view_sumsq_kernel<<<m, 1024, 0, st>>>(reinterpret_cast<const float2*>(spectra), (size_t)C * Hp * Whp,
-                                          view_sumsq);
-    FDL_LAUNCH_CHECK("view_sumsq_kernel");
+    double* partial = reinterpret_cast<double*>(reinterpret_cast<char*>(fft_work) + align256(plan->work));
+    view_sumsq_partial_kernel<<<m * SUMSQ_SPLIT, 512, 0, st>>>(reinterpret_cast<const float2*>(spectra),
+                                                              (size_t)C * Hp * Whp, partial);
+    FDL_LAUNCH_CHECK("view_sumsq_partial_kernel");
+    view_sumsq_final_kernel<<<(m + 127) / 128, 128, 0, st>>>(partial, m, view_sumsq);
+    FDL_LAUNCH_CHECK("view_sumsq_final_kernel");
   }
   return FDL_OK;
 }

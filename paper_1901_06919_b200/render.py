@@ -295,19 +295,29 @@ def render_many_device(model: FdlModel, reqs, batch: int = 64):
     return out, oob
 
 
-def _to_numpy_images(imgs):
-    arr = imgs.cpu().numpy().astype(np.float64)
+def _to_numpy_images(imgs, dtype=np.float64):
+    """CUDA (V,H,W,C) float32 -> numpy (V,H,W[,C]) of `dtype`: cast on the device,
+    one D2H copy into pinned memory (torch's caching host allocator), no host
+    conversion pass."""
+    import torch
+    tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+    dev = imgs.to(tdt)
+    host = torch.empty(dev.shape, dtype=tdt, pin_memory=True)
+    host.copy_(dev, non_blocking=True)
+    torch.cuda.current_stream(imgs.device).synchronize()
+    arr = host.numpy()
     if arr.shape[-1] == 1:
         arr = arr[..., 0]
     return arr
 
 
-def render_many(model: FdlModel, reqs, batch: int = 64) -> list[np.ndarray]:
-    """Batched `render`: one float64 image per request; stats describe the last request."""
+def render_many(model: FdlModel, reqs, batch: int = 64, dtype=np.float64) -> list[np.ndarray]:
+    """Batched `render`: one image per request (float64 like the reference, or
+    float32 with dtype=np.float32); stats describe the last request."""
     t0 = time.perf_counter()
     reqs = list(reqs)
     imgs, oob = render_many_device(model, reqs, batch)
-    host = _to_numpy_images(imgs)
+    host = _to_numpy_images(imgs, dtype)
     oob_h = oob.cpu().numpy()
     for r, cnt in zip(reqs, oob_h):
         if _uses_aperture(r):
@@ -322,7 +332,7 @@ def render_many(model: FdlModel, reqs, batch: int = 64) -> list[np.ndarray]:
     st.layer_ops = model.num_layers * q * (3 if st.aperture_pass else 2)
     st.oob_lookups = int(oob_h[-1]) if st.aperture_pass else 0
     st.seconds = time.perf_counter() - t0
-    return [np.ascontiguousarray(h) for h in host]
+    return list(host)
 
 
 def render(model: FdlModel, req: RenderRequest) -> np.ndarray:
