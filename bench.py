@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=24)
+    ap.add_argument("--c5-views", type=int, default=256, help="config 5: views rendered per step and rank")
     return ap.parse_args()
 
 
@@ -134,6 +135,59 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- our arm
+def run_c5(args, rank, world, device):
+    """Config 5: render-only sweep over a precomputed random FDL (64 layers, 1920x1080 RGB)."""
+    import importlib
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_06919_b200 as fdl
+    from harness.synth import random_fdl_layers, render_requests_c5
+    R = importlib.import_module("paper_1901_06919_b200.render")
+    H, W, n, C = (args.size or 1080), (int(args.size * 16 / 9) if args.size else 1920), 64, 3
+    layers = random_fdl_layers(n, C, H, W, device=device)
+    d = np.linspace(-5, 5, n)
+    model = fdl.FdlModel(disparities=d, layers=layers, grid=fdl.FrequencyGrid(W, H), width=W, height=H)
+    per_step = args.c5_views
+    u, v, s, f = render_requests_c5(per_step * world)
+    ap = fdl.aperture_spectrum("disk", diameter=1.0)
+    reqs = [fdl.RenderRequest(u=u[i], v=v[i], s=s[i], f=f[i], aperture=ap) for i in range(len(u))]
+    mine = reqs[rank * per_step:(rank + 1) * per_step]
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        R.render_many_device(model, mine, batch=args.batch)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(device.index or 0)
+    sampler.start()
+    torch.cuda.nvtx.range_push("timed")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        R.render_many_device(model, mine, batch=args.batch)
+    e1.record(stream)
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    t = e0.elapsed_time(e1) / 1e3 / args.steps
+    if world > 1:
+        tt = torch.tensor([t], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    Q = H * (W // 2 + 1)
+    flops_view = Q * n * (8 * C + 6 + 8)
+    return {"metric": "rendered views/s (config 5)", "value": world * per_step / t, "unit": "views/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 render",
+            "data": "synthetic random FDL (harness/synth.py random_fdl_layers, render_requests_c5)",
+            "config": {"workload": f"c5: render {per_step} views/rank of a {n}-layer {W}x{H}x{C} FDL, disk(1) f=2r",
+                       "views_per_step": per_step * world},
+            "render_flops_tf": flops_view * per_step / t / 1e12,
+            "clocks": clocks, "gpu_launches": args.steps * 4 * math.ceil(per_step / args.batch)}
+
+
 def run_ours(args, rank, world, device):
     import torch
     import torch.distributed as dist
@@ -413,6 +467,14 @@ def main():
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
+    if args.config == "c5":
+        res = run_c5(args, rank, world, device)
+        if rank == 0:
+            print(json.dumps(res))
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     res, case, dims = run_ours(args, rank, world, device)
     if not args.no_e2e and world == 1:
         res["e2e"] = run_e2e(args, case, dims, device)
