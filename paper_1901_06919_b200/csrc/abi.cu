@@ -409,16 +409,35 @@ int plan_render(const fdl_render_desc* D, RenderPlan& P) {
   for (int a = 0; a < nap; ++a) {
     const fdl_aperture& ap = D->apertures[a];
     if (ap.rows < 2 || ap.cols < 2 || !ap.table_re) return fail(FDL_ERR_INVALID, "aperture table needs >= 2x2 entries");
-    size_t cnt = (size_t)ap.rows * ap.cols;
-    std::vector<float> tmp(cnt);
-    for (size_t e = 0; e < cnt; ++e) tmp[e] = (float)ap.table_re[e];
-    P.o_re.push_back(B.add(tmp.data(), cnt * sizeof(float)));
+    const size_t R = ap.rows, Cc = ap.cols, cnt = R * Cc;
+    std::vector<float> quad(4 * (cnt + 1), 0.0f);
+    auto build = [&](const double* T) {
+      std::fill(quad.begin(), quad.end(), 0.0f);
+      for (size_t iy = 0; iy + 1 < R; ++iy)
+        for (size_t ix = 0; ix + 1 < Cc; ++ix) {
+          float* e = &quad[4 * (iy * Cc + ix)];
+          e[0] = (float)T[iy * Cc + ix];
+          e[1] = (float)T[iy * Cc + ix + 1];
+          e[2] = (float)T[(iy + 1) * Cc + ix];
+          e[3] = (float)T[(iy + 1) * Cc + ix + 1];
+        }
+    };
+    build(ap.table_re);
+    P.o_re.push_back(B.add(quad.data(), quad.size() * sizeof(float)));
     if (ap.table_im) {
-      for (size_t e = 0; e < cnt; ++e) tmp[e] = (float)ap.table_im[e];
-      P.o_im.push_back(B.add(tmp.data(), cnt * sizeof(float)));
+      build(ap.table_im);
+      P.o_im.push_back(B.add(quad.data(), quad.size() * sizeof(float)));
     } else {
       P.o_im.push_back((size_t)-1);
     }
+  }
+  // every view of the batch on the same real table -> uniform fast path
+  p.uniform_ap = -1;
+  if (D->view_aperture && V > 0) {
+    const int a0 = vap[0];
+    bool uni = a0 >= 0 && !D->apertures[a0].table_im;
+    for (int v = 1; v < V && uni; ++v) uni = vap[v] == a0;
+    if (uni) p.uniform_ap = a0;
   }
   return FDL_OK;
 }
@@ -454,8 +473,9 @@ void bind_render(RenderPlan& P, const fdl_render_desc* D, void* ws) {
     RenderTable rt;
     rt.rows = ap.rows;
     rt.cols = ap.cols;
-    rt.re = at<float>(ws, P.o_re[a]);
-    rt.im = P.o_im[a] == (size_t)-1 ? nullptr : at<float>(ws, P.o_im[a]);
+    rt.zero = ap.rows * ap.cols;
+    rt.re = at<float4>(ws, P.o_re[a]);
+    rt.im = P.o_im[a] == (size_t)-1 ? nullptr : at<float4>(ws, P.o_im[a]);
     htab[a] = rt;
   }
   char* base = reinterpret_cast<char*>(ws) + P.blob.size();

@@ -9,6 +9,8 @@
 // (view, bin, layer), one complex product of the two axis phases, an optional
 // 2x2 bilinear gather from the float32 table and the complex MAC over
 // channels, all in float32 (>= 83 dB).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "k3_render.cuh"
 
@@ -43,7 +45,7 @@ __global__ void render_factors_kernel(RenderParams p) {
       int i0;
       double fr;
       bool ok = axis_lookup(t * ox, ap.xi0_x, ap.step_x, ap.cols, i0, fr);
-      f.idx = ok ? i0 : -1;
+      f.idx = ok ? i0 : ap.rows * ap.cols;  // quad-table column; out of range -> the zero entry
       f.frac = (float)fr;
       bad_x += ok ? 0 : 1;
     }
@@ -65,7 +67,7 @@ __global__ void render_factors_kernel(RenderParams p) {
       int i0;
       double fr;
       bool ok = axis_lookup(t * oy, ap.xi0_y, ap.step_y, ap.rows, i0, fr);
-      f.idx = ok ? i0 : -1;
+      f.idx = ok ? i0 * ap.cols : ap.rows * ap.cols;  // quad-table row offset
       f.frac = (float)fr;
       bad_y += ok ? 0 : 1;
     }
@@ -102,7 +104,12 @@ constexpr int TX = 32, TY = 8;
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
   const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
   const int src_size = valid ? 16 : 0;  // 0: zero-fill (weight 0)
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gsrc), "r"(src_size));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gsrc), "r"(src_size));
+}
+__device__ __forceinline__ float2 ld_stream(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -110,7 +117,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 constexpr int NSTAGE = 3;  // factor ring: layer k in use, k+1 and k+2 in flight
 
-template <int C, int VB, bool AP>
+template <int C, int VB, bool AP, bool UNI>
 __global__ void __launch_bounds__(TX * TY, 2) render_tile_kernel(RenderParams p) {
   __shared__ __align__(16) AxisFactor FX[NSTAGE][VB][TX];
   __shared__ __align__(16) AxisFactor FY[NSTAGE][VB][TY];
@@ -145,7 +152,14 @@ __global__ void __launch_bounds__(TX * TY, 2) render_tile_kernel(RenderParams p)
   };
 
   __shared__ int TIDX[VB];
-  if (tid < VB) TIDX[tid] = (AP && tid < nv && p.view_ap) ? p.view_ap[v0 + tid] : -1;
+  __shared__ RenderTable TB[VB];
+  if (tid < VB) {
+    const int ai = (AP && tid < nv && p.view_ap) ? p.view_ap[v0 + tid] : -1;
+    TIDX[tid] = ai;
+    if (ai >= 0) TB[tid] = p.tables[ai];
+  }
+  RenderTable tb0{};
+  if (UNI) tb0 = p.tables[p.uniform_ap];
   // (made visible by the first __syncthreads of the layer loop)
 
   float2 acc[VB][C];
@@ -156,27 +170,21 @@ __global__ void __launch_bounds__(TX * TY, 2) render_tile_kernel(RenderParams p)
 
   float2 Lnext[C];
 #pragma unroll
-  for (int c = 0; c < C; ++c) Lnext[c] = inside ? __ldg(p.layers + (size_t)c * Q + q) : make_float2(0.f, 0.f);
+  for (int c = 0; c < C; ++c) Lnext[c] = inside ? ld_stream(p.layers + (size_t)c * Q + q) : make_float2(0.f, 0.f);
   stage(0);
   if (p.n > 1) stage(1);
   for (int k = 0; k < p.n; ++k) {
     const int buf = k % NSTAGE;
-    if (k + 2 < p.n) {
-      stage(k + 2);
-      cp_async_wait<2>();
-    } else if (k + 1 < p.n) {
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();  // layer k's factors visible to all threads
+    cp_async_wait<0>();  // layers k and k+1 staged (k+1 was issued one layer ago)
+    __syncthreads();     // ... and visible; everyone is done with layer k-1's buffer
+    if (k + 2 < p.n) stage(k + 2);
     float2 L[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) L[c] = Lnext[c];
     if (k + 1 < p.n) {
 #pragma unroll
       for (int c = 0; c < C; ++c)
-        Lnext[c] = inside ? __ldg(p.layers + ((size_t)(k + 1) * C + c) * Q + q) : make_float2(0.f, 0.f);
+        Lnext[c] = inside ? ld_stream(p.layers + ((size_t)(k + 1) * C + c) * Q + q) : make_float2(0.f, 0.f);
     }
     const AxisFactor* fxp = &FX[buf][0][tx];
     const AxisFactor* fyp = &FY[buf][0][ty];
@@ -186,30 +194,27 @@ __global__ void __launch_bounds__(TX * TY, 2) render_tile_kernel(RenderParams p)
       const AxisFactor fy = fyp[b * TY];
       float wr = fy.re * fx.re - fy.im * fx.im;
       float wi = fy.re * fx.im + fy.im * fx.re;
-      const int ai = AP ? TIDX[b] : -1;
+      const int ai = UNI ? p.uniform_ap : (AP ? TIDX[b] : -1);
       if (AP && ai >= 0) {
-        const RenderTable tb = p.tables[ai];
-        if (fx.idx < 0 || fy.idx < 0) {
-          wr = 0.f;
-          wi = 0.f;
+        // one 16-byte quad-table load; out-of-range rows/columns hit the zero entry.
+        // separable passes of lfmodel.py:115-116: rows (fy) first, then columns (fx)
+        const RenderTable& tb = UNI ? tb0 : TB[b];
+        const int qi = min(fy.idx + fx.idx, tb.zero);
+        const float4 tr = __ldg(tb.re + qi);
+        const float top = fmaf(fy.frac, tr.z - tr.x, tr.x);
+        const float bot = fmaf(fy.frac, tr.w - tr.y, tr.y);
+        const float sr = fmaf(fx.frac, bot - top, top);
+        if (!UNI && tb.im) {
+          const float4 ti = __ldg(tb.im + qi);
+          const float tt = fmaf(fy.frac, ti.z - ti.x, ti.x);
+          const float bb = fmaf(fy.frac, ti.w - ti.y, ti.y);
+          const float si = fmaf(fx.frac, bb - tt, tt);
+          const float nr = wr * sr - wi * si;
+          wi = wr * si + wi * sr;
+          wr = nr;
         } else {
-          const size_t r0 = (size_t)fy.idx * tb.cols + fx.idx, r1 = r0 + tb.cols;
-          const float gx = fx.frac, gy = fy.frac;
-          // separable passes of lfmodel.py:115-116: rows first, then columns
-          const float top = __ldg(tb.re + r0) * (1.f - gy) + __ldg(tb.re + r1) * gy;
-          const float bot = __ldg(tb.re + r0 + 1) * (1.f - gy) + __ldg(tb.re + r1 + 1) * gy;
-          const float sr = top * (1.f - gx) + bot * gx;
-          if (tb.im) {
-            const float ti = __ldg(tb.im + r0) * (1.f - gy) + __ldg(tb.im + r1) * gy;
-            const float bi = __ldg(tb.im + r0 + 1) * (1.f - gy) + __ldg(tb.im + r1 + 1) * gy;
-            const float si = ti * (1.f - gx) + bi * gx;
-            const float nr = wr * sr - wi * si;
-            wi = wr * si + wi * sr;
-            wr = nr;
-          } else {
-            wr *= sr;
-            wi *= sr;
-          }
+          wr *= sr;
+          wi *= sr;
         }
       }
 #pragma unroll
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(TX * TY, 2) render_pin_kernel(RenderParams p) 
     for (int c = 0; c < C; ++c) acc[b][c] = make_float2(0.f, 0.f);
   float2 Lnext[C];
 #pragma unroll
-  for (int c = 0; c < C; ++c) Lnext[c] = inside ? __ldg(p.layers + (size_t)c * Q + q) : make_float2(0.f, 0.f);
+  for (int c = 0; c < C; ++c) Lnext[c] = inside ? ld_stream(p.layers + (size_t)c * Q + q) : make_float2(0.f, 0.f);
   stage(0);
   if (p.n > 1) stage(1);
   const float2* lp = p.layers + q;  // + (k * C + c) * Q
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(TX * TY, 2) render_pin_kernel(RenderParams p) 
     if (k + 1 < p.n) {
 #pragma unroll
       for (int c = 0; c < C; ++c)
-        Lnext[c] = inside ? __ldg(lp + ((size_t)(k + 1) * C + c) * Q) : make_float2(0.f, 0.f);
+        Lnext[c] = inside ? ld_stream(lp + ((size_t)(k + 1) * C + c) * Q) : make_float2(0.f, 0.f);
     }
     const float4* fxp = &FX2[buf][0][tx];
     const float4* fyp = &FY2[buf][0][ty];
@@ -321,14 +326,33 @@ __global__ void __launch_bounds__(TX * TY, 2) render_pin_kernel(RenderParams p) 
   }
 }
 
+template <int C, int VB>
+void launch_ap(const RenderParams& p, dim3 grid, dim3 block, cudaStream_t st) {
+  if (p.uniform_ap >= 0)  // every view on one real table
+    render_tile_kernel<C, VB, true, true><<<grid, block, 0, st>>>(p);
+  else  // mixed batch: per-view tables (real or complex)
+    render_tile_kernel<C, VB, true, false><<<grid, block, 0, st>>>(p);
+}
+
+int render_vb_env() {
+  static int vb = [] {
+    const char* e = getenv("FDL_RENDER_VB");
+    return e ? atoi(e) : 16;
+  }();
+  return vb;
+}
+
 template <int C>
 int launch_sum(const RenderParams& p, cudaStream_t st) {
   constexpr int VB = C <= 3 ? 16 : 8;
   dim3 block(TX, TY);
   dim3 grid((unsigned)((p.Whp + TX - 1) / TX), (unsigned)((p.Hp + TY - 1) / TY), (unsigned)((p.V + VB - 1) / VB));
-  if (p.view_ap)  // some view of the batch has an aperture: the per-view check is inside
-    render_tile_kernel<C, VB, true><<<grid, block, 0, st>>>(p);
-  else
+  if (p.view_ap && VB == 16 && render_vb_env() == 8) {
+    dim3 g8(grid.x, grid.y, (unsigned)((p.V + 7) / 8));
+    launch_ap<C, 8>(p, g8, block, st);
+  } else if (p.view_ap) {
+    launch_ap<C, VB>(p, grid, block, st);
+  } else
     render_pin_kernel<C, VB><<<grid, block, 0, st>>>(p);
   FDL_LAUNCH_CHECK("render_tile_kernel");
   return FDL_OK;

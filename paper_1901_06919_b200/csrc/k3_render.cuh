@@ -9,13 +9,18 @@ struct __align__(16) AxisFactor {
   int idx;
 };
 
+// Aperture table for the render hot loop: "quad" layout, entry (iy, ix) holds
+// (T[iy][ix], T[iy][ix+1], T[iy+1][ix], T[iy+1][ix+1]) so one 16-byte load
+// feeds a bilinear lookup; entry `zero` (= rows * cols) is all zeros and is
+// where out-of-range lookups point (lfmodel.py:118-121 sets them to 0).
 struct RenderTable {
-  int rows, cols;
-  const float* re;
-  const float* im;  // nullptr for a real table
+  int rows, cols, zero;
+  const float4* re;
+  const float4* im;  // nullptr for a real table
 };
 
 struct RenderParams {
+  int uniform_ap;          // >= 0: every view of the batch uses this real table (fast path)
   int n, C, Hp, Wp, Whp, V;
   const double* pu;        // (V, n)
   const double* pv;        // (V, n)
