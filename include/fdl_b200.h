@@ -139,6 +139,34 @@ int fdl_solve_bins(const fdl_solve_desc* desc, void* workspace_dev, size_t works
 /* Which path fdl_solve_bins picks for this descriptor (1, 2, 3 as force_path). */
 int fdl_solve_path(const fdl_solve_desc* desc);
 
+/* Re-solve the bins fdl_solve_bins flagged (FDL_BIN_BREAKDOWN) with the
+ * reference's minimum-norm fallback `_stacked_lstsq` (construct.py:157-165,
+ * 205-210): A, b and reg of each listed bin are rebuilt on the device and
+ * [A; sqrt(lam reg)] x = [b; 0] is solved by an fp64 Jacobi SVD.  bins is a
+ * HOST array of flat slab bin indices (row * Whp + kx).  lam must be > 0. */
+size_t fdl_resolve_bins_workspace(const fdl_solve_desc* desc, int32_t nbins);
+int fdl_resolve_bins(const fdl_solve_desc* desc, const int32_t* bins, int32_t nbins, void* workspace_dev,
+                     size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Explicit per-bin systems   (solve_frequency, construct.py:123-165)        */
+/* ------------------------------------------------------------------------ */
+
+typedef struct fdl_dense_desc {
+  int32_t batch, m, n, C;      /* problems, rows, unknowns (<= 64), right-hand sides */
+  const void* A_dev;           /* (batch, m, n) complex128 */
+  const void* b_dev;           /* (batch, m, C) complex128 */
+  const double* reg_dev;       /* (batch, n) diagonal regulariser, or NULL */
+  const void* R_dev;           /* (batch, n, n) complex128 Hermitian regulariser, or NULL */
+  double lam;                  /* >= 0 */
+  void* x_dev;                 /* (batch, n, C) complex128 */
+  int8_t* status_dev;          /* (batch): 0 normal equations accepted, 2 minimum-norm fallback used,
+                                  1 fallback failed, 3 singular / inaccurate at lam = 0 */
+} fdl_dense_desc;
+
+size_t fdl_solve_dense_workspace(const fdl_dense_desc* desc);
+int fdl_solve_dense(const fdl_dense_desc* desc, void* workspace_dev, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* K2: conjugate-pair symmetrisation of self-conjugate columns (construct.py:286-297) */
 /* ------------------------------------------------------------------------ */

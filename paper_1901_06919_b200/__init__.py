@@ -13,7 +13,9 @@ from .construct import (
     DEFAULT_EPS,
     SOLVE_CHUNK,
     RankDeficiencyError,
+    build_system_row,
     construct_fdl,
+    solve_frequency,
     default_lambda,
     last_construct_stats,
     view_regularizer,
@@ -45,7 +47,9 @@ __all__ = [
     "DEFAULT_EPS",
     "SOLVE_CHUNK",
     "RankDeficiencyError",
+    "build_system_row",
     "construct_fdl",
+    "solve_frequency",
     "default_lambda",
     "last_construct_stats",
     "view_regularizer",

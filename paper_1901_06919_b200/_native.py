@@ -66,6 +66,15 @@ class FdlRenderDesc(ctypes.Structure):
     ]
 
 
+class FdlDenseDesc(ctypes.Structure):
+    _fields_ = [
+        ("batch", ctypes.c_int32), ("m", ctypes.c_int32), ("n", ctypes.c_int32), ("C", ctypes.c_int32),
+        ("A_dev", ctypes.c_void_p), ("b_dev", ctypes.c_void_p), ("reg_dev", ctypes.c_void_p),
+        ("R_dev", ctypes.c_void_p), ("lam", ctypes.c_double), ("x_dev", ctypes.c_void_p),
+        ("status_dev", ctypes.c_void_p),
+    ]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -82,6 +91,12 @@ EXPORTS = {
     "fdl_solve_bins": (ctypes.c_int, [ctypes.POINTER(FdlSolveDesc), ctypes.c_void_p, ctypes.c_size_t,
                                       c_int32_p, ctypes.c_void_p]),
     "fdl_solve_path": (ctypes.c_int, [ctypes.POINTER(FdlSolveDesc)]),
+    "fdl_resolve_bins_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlSolveDesc), ctypes.c_int32]),
+    "fdl_resolve_bins": (ctypes.c_int, [ctypes.POINTER(FdlSolveDesc), c_int32_p, ctypes.c_int32, ctypes.c_void_p,
+                                        ctypes.c_size_t, ctypes.c_void_p]),
+    "fdl_solve_dense_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlDenseDesc)]),
+    "fdl_solve_dense": (ctypes.c_int, [ctypes.POINTER(FdlDenseDesc), ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.c_void_p]),
     "fdl_symmetrize": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 5 + [
         c_int32_p, c_int32_p, ctypes.c_void_p]),
     "fdl_render_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlRenderDesc)]),

@@ -24,6 +24,9 @@ from .spectra import FrequencyGrid
 
 __all__ = [
     "RankDeficiencyError",
+    "build_system_row",
+    "solve_frequency",
+    "solve_dense",
     "DEFAULT_EPS",
     "SOLVE_CHUNK",
     "view_regularizer",
@@ -47,17 +50,120 @@ def view_regularizer(omega_x, omega_y, d, eps: float = DEFAULT_EPS):
     return w4[..., None] * np.asarray(d, float) ** 4 + eps
 
 
+def build_system_row(view: ViewSet, j: int, omega, d, grid: FrequencyGrid | None = None):
+    """System-matrix row of view j at frequency (wx, wy) (construct.py:83-109).
+
+    A host helper (one row, n entries) with the reference's Nyquist handling;
+    the construction itself generates A on the device.
+    """
+    wx, wy = float(omega[0]), float(omega[1])
+    d = np.asarray(d, dtype=np.float64)
+    pu, pv = view.u[j] * d, view.v[j] * d
+    phx = np.exp(2j * np.pi * pu * wx)
+    phy = np.exp(2j * np.pi * pv * wy)
+    if grid is not None:
+        if grid.width % 2 == 0 and wx == grid.omega_x[grid.width // 2]:
+            phx = np.cos(np.pi * pu).astype(np.complex128)
+        if grid.height % 2 == 0 and wy == grid.omega_y[grid.height // 2]:
+            phy = np.cos(np.pi * pv).astype(np.complex128)
+    row = phx * phy
+    ap = view.apertures[j]
+    if ap is not None and not ap.is_pinhole:
+        t = view.aperture_scale[j] * (view.s[j] - d)
+        row = row * ap.evaluate(t * wx, t * wy)
+    return row
+
+
+def solve_dense(A, b, reg, lam: float, device=None):
+    """Batched explicit regularised solves on the GPU (fdl_solve_dense).
+
+    A (B, m, n), b (B, m, C), reg (B, n) diagonal or (B, n, n) Hermitian.
+    Returns (x (B, n, C) complex128 numpy, status (B,) int8): 0 normal
+    equations accepted, 2 minimum-norm fallback used, 1 failed, 3 singular at lam = 0.
+    """
+    torch = _require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    A = np.ascontiguousarray(A, dtype=np.complex128)
+    b = np.ascontiguousarray(b, dtype=np.complex128)
+    B, m, n = A.shape
+    C = b.shape[2]
+    reg = np.asarray(reg)
+    At = torch.from_numpy(A).to(dev)
+    bt = torch.from_numpy(b).to(dev)
+    x = torch.empty((B, n, C), dtype=torch.complex128, device=dev)
+    status = torch.zeros(B, dtype=torch.int8, device=dev)
+    desc = nat.FdlDenseDesc()
+    desc.batch, desc.m, desc.n, desc.C = B, m, n, C
+    desc.A_dev, desc.b_dev, desc.x_dev, desc.status_dev = At.data_ptr(), bt.data_ptr(), x.data_ptr(), status.data_ptr()
+    keep = []
+    if reg.ndim == 2 and reg.shape == (B, n):
+        rt = torch.from_numpy(np.ascontiguousarray(reg, dtype=np.float64)).to(dev)
+        desc.reg_dev = rt.data_ptr()
+        keep.append(rt)
+    else:
+        Rt = torch.from_numpy(np.ascontiguousarray(reg, dtype=np.complex128)).to(dev)
+        desc.R_dev = Rt.data_ptr()
+        keep.append(Rt)
+    desc.lam = float(lam)
+    L = nat.lib()
+    ws = nat.workspace(L.fdl_solve_dense_workspace(desc), dev)
+    nat.check(L.fdl_solve_dense(desc, ws.data_ptr(), ws.numel(), nat.stream_handle(dev)), "fdl_solve_dense")
+    return x.cpu().numpy(), status.cpu().numpy()
+
+
+def _reg_matrix(reg, n):
+    """construct.py:112-120 (validation of the regulariser argument)."""
+    reg = np.asarray(reg, dtype=np.float64) if np.isrealobj(reg) else np.asarray(reg)
+    if reg.ndim == 1:
+        if reg.shape != (n,):
+            raise ValueError("diagonal regularizer length must equal layer count")
+        return reg
+    if reg.shape != (n, n):
+        raise ValueError("regularizer must be an n-vector or n x n matrix")
+    return reg
+
+
+def solve_frequency(A, b, reg, lam: float, freq=None):
+    """x = (A*A + lam reg)^-1 A*b for one frequency (construct.py:123-154), on the GPU.
+
+    Same contract as the reference: the normal-equation residual is below
+    1e-8 relative, a degenerate system with lam > 0 falls back to the
+    minimum-norm stacked least squares, lam = 0 raises RankDeficiencyError
+    when the system is singular or over-parameterised.
+    """
+    A = np.asarray(A, dtype=np.complex128)
+    b = np.asarray(b, dtype=np.complex128)
+    m, n = A.shape
+    if lam < 0:
+        raise ValueError("lam must be non-negative")
+    if lam == 0 and n > m:
+        raise RankDeficiencyError(f"{n} layers from {m} images is ill-posed without regularization")
+    R = _reg_matrix(reg, n)
+    vec = b.ndim == 1
+    bb = b.reshape(m, -1)
+    Rb = R[None] if R.ndim == 2 else R[None, :]
+    x, status = solve_dense(A[None], bb[None], Rb, lam)
+    tag = "" if freq is None else f" at frequency {freq}"
+    if status[0] == 3:
+        raise RankDeficiencyError(f"singular normal matrix{tag}")
+    if status[0] == 1:
+        raise nat.FdlNativeError(f"minimum-norm fallback failed{tag}")
+    out = x[0]
+    return out[:, 0] if vec else out
+
+
 def default_lambda(b_norms_sq, m: int) -> float:
     """1e-4 * mean_q ||b_q||^2 / m (construct.py:214-216)."""
     return 1e-4 * float(np.mean(b_norms_sq)) / m
 
 
 class ConstructStats:
-    """Breakdown of the last construct_fdl call on this thread (host seconds)."""
+    """What the last construct_fdl call on this thread did."""
 
     def __init__(self):
-        self.path = 0
-        self.breakdown_bins = 0
+        self.path = 0              # K1 formulation: 1 symmetric-real, 2 real-A, 3 complex
+        self.breakdown_bins = 0    # bins left unsolved
+        self.fallback_bins = 0     # bins re-solved by the minimum-norm fallback
         self.lam = None
 
 
@@ -163,7 +269,17 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     nb = nat.ctypes.c_int32(0)
     nat.check(L.fdl_solve_bins(desc, ws.data_ptr(), ws.numel(), nat.ctypes.byref(nb),
                                nat.stream_handle(device)), "fdl_solve_bins")
-    return layers, int(nb.value), path
+    n_bad = int(nb.value)
+    if n_bad and lam > 0:
+        # the reference's minimum-norm fallback for the flagged bins (construct.py:205-210), on the GPU
+        bins = np.ascontiguousarray(np.flatnonzero(status.cpu().numpy().reshape(-1)), dtype=np.int32)
+        rws = nat.workspace(L.fdl_resolve_bins_workspace(desc, len(bins)), device)
+        nat.check(L.fdl_resolve_bins(desc, nat.iptr(bins), len(bins), rws.data_ptr(), rws.numel(),
+                                     nat.stream_handle(device)), "fdl_resolve_bins")
+        n_bad = int(torch.count_nonzero(status).item())
+    st = last_construct_stats()
+    st.fallback_bins = int(nb.value) - n_bad
+    return layers, n_bad, path
 
 
 def views_to_spectra(views_dev, pad):
@@ -260,7 +376,7 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
     if n_bad:
         if lam == 0:
             raise RankDeficiencyError("singular normal matrix at some frequency")
-        raise nat.FdlNativeError(f"{n_bad} bins broke down in the fp64 Cholesky (min-norm fallback pending)")
+        raise nat.FdlNativeError(f"{n_bad} bins could not be solved (minimum-norm fallback failed)")
     symmetrize(layers, Hp, Wp)
     return FdlModel(disparities=d, layers=layers, grid=grid, width=W, height=H, pad_margin=pad_margin,
                     color_space=views.color_space, calibration=shifts, lambda_used=float(lam))

@@ -25,6 +25,14 @@ int spectra_to_images(fdl_c64* spectra, int V, int C, int Hp, int Wp, int pad, i
 int k1_generic_launch(const SolveParams& p, cudaStream_t st);
 int k1_fast_launch(const SolveParams& p, cudaStream_t st, bool* handled);
 int selftest_dmma(cudaStream_t st, double* max_err);
+size_t dense_scratch_doubles(int m, int n, int C);
+int dense_solve_launch(int batch, int m, int n, int C, const double2* A, const double2* b, const double* reg,
+                       const double2* R, double lam, double2* x, signed char* status, signed char* status2,
+                       double* scratch, bool force_minnorm, cudaStream_t st);
+int build_bins_launch(const SolveParams& p, const int* bins, int nb, double2* A, double2* b, double* reg,
+                      cudaStream_t st);
+int scatter_bins_launch(const SolveParams& p, const int* bins, int nb, const double2* x, const signed char* st2,
+                        cudaStream_t st);
 
 // --- errors --------------------------------------------------------------------
 thread_local std::string t_error;
@@ -580,6 +588,88 @@ int fdl_solve_bins(const fdl_solve_desc* desc, void* workspace_dev, size_t works
     }
   }
   return FDL_OK;
+}
+
+namespace {
+// resolve workspace: [blob][bins int][A c128][b c128][reg f64][x c128][status][scratch f64]
+struct ResolveLayout {
+  size_t bins, A, b, reg, x, st, scratch, total;
+};
+ResolveLayout resolve_layout(size_t base, int m, int n, int C, int nb) {
+  ResolveLayout L;
+  size_t o = align256(base);
+  L.bins = o; o = align256(o + sizeof(int) * nb);
+  L.A = o; o = align256(o + 16 * (size_t)nb * m * n);
+  L.b = o; o = align256(o + 16 * (size_t)nb * m * C);
+  L.reg = o; o = align256(o + 8 * (size_t)nb * n);
+  L.x = o; o = align256(o + 16 * (size_t)nb * n * C);
+  L.st = o; o = align256(o + (size_t)nb);
+  L.scratch = o; o = align256(o + 8 * (size_t)nb * dense_scratch_doubles(m, n, C));
+  L.total = o;
+  return L;
+}
+}  // namespace
+
+size_t fdl_resolve_bins_workspace(const fdl_solve_desc* desc, int32_t nbins) {
+  SolvePlan P;
+  int mode;
+  if (plan_solve(desc, P, &mode)) return 0;
+  return resolve_layout(P.ws_bytes(), desc->m, desc->n, desc->C, nbins).total;
+}
+
+int fdl_resolve_bins(const fdl_solve_desc* desc, const int32_t* bins, int32_t nbins, void* workspace_dev,
+                     size_t workspace_bytes, void* stream) {
+  SolvePlan P;
+  int mode;
+  int rc = plan_solve(desc, P, &mode);
+  if (rc) return rc;
+  if (nbins < 0 || (nbins > 0 && !bins)) return fail(FDL_ERR_INVALID, "invalid bin list");
+  if (!(desc->lam > 0.0)) return fail(FDL_ERR_RANK, "singular normal matrix (lam = 0)");
+  const ResolveLayout L = resolve_layout(P.ws_bytes(), desc->m, desc->n, desc->C, nbins);
+  if (workspace_bytes < L.total || !workspace_dev) return fail(FDL_ERR_INVALID, "workspace too small for fdl_resolve_bins");
+  if (nbins == 0) return FDL_OK;
+  const long long nb_all = (long long)desc->nrows * (desc->Wp / 2 + 1);
+  for (int i = 0; i < nbins; ++i)
+    if (bins[i] < 0 || bins[i] >= nb_all) return fail(FDL_ERR_INVALID, "bin index out of range");
+  cudaStream_t st = as_stream(stream);
+  char* ws = reinterpret_cast<char*>(workspace_dev);
+  bind_solve(P, desc, workspace_dev);
+  rc = upload(P.blob, workspace_dev, st);
+  if (rc) return rc;
+  Blob bb;
+  bb.add(bins, sizeof(int) * nbins);
+  rc = upload(bb, ws + L.bins, st);
+  if (rc) return rc;
+  const int* dbins = reinterpret_cast<const int*>(ws + L.bins);
+  double2* A = reinterpret_cast<double2*>(ws + L.A);
+  double2* b = reinterpret_cast<double2*>(ws + L.b);
+  double* reg = reinterpret_cast<double*>(ws + L.reg);
+  double2* x = reinterpret_cast<double2*>(ws + L.x);
+  signed char* s2 = reinterpret_cast<signed char*>(ws + L.st);
+  rc = build_bins_launch(P.p, dbins, nbins, A, b, reg, st);
+  if (rc) return rc;
+  rc = dense_solve_launch(nbins, desc->m, desc->n, desc->C, A, b, reg, nullptr, desc->lam, x, s2, s2,
+                          reinterpret_cast<double*>(ws + L.scratch), true, st);
+  if (rc) return rc;
+  return scatter_bins_launch(P.p, dbins, nbins, x, s2, st);
+}
+
+size_t fdl_solve_dense_workspace(const fdl_dense_desc* d) {
+  if (!d || d->batch < 0 || d->m < 1 || d->n < 1 || d->C < 1) return 0;
+  return align256(8 * (size_t)d->batch * dense_scratch_doubles(d->m, d->n, d->C)) + 256;
+}
+
+int fdl_solve_dense(const fdl_dense_desc* d, void* workspace_dev, size_t workspace_bytes, void* stream) {
+  if (!d || d->batch < 0 || d->m < 1 || d->n < 1 || d->C < 1) return fail(FDL_ERR_INVALID, "invalid dense system");
+  if (!(d->lam >= 0.0) || !std::isfinite(d->lam)) return fail(FDL_ERR_INVALID, "lam must be non-negative");
+  if (!d->A_dev || !d->b_dev || !d->x_dev || !d->status_dev) return fail(FDL_ERR_INVALID, "null buffer");
+  if (workspace_bytes < fdl_solve_dense_workspace(d) || !workspace_dev)
+    return fail(FDL_ERR_INVALID, "workspace too small for fdl_solve_dense");
+  return dense_solve_launch(d->batch, d->m, d->n, d->C, reinterpret_cast<const double2*>(d->A_dev),
+                            reinterpret_cast<const double2*>(d->b_dev), d->reg_dev,
+                            reinterpret_cast<const double2*>(d->R_dev), d->lam, reinterpret_cast<double2*>(d->x_dev),
+                            d->status_dev, d->status_dev, reinterpret_cast<double*>(workspace_dev), false,
+                            as_stream(stream));
 }
 
 int fdl_symmetrize(fdl_c64* layers_dev, int32_t n, int32_t C, int32_t Hp, int32_t Wp, int32_t nrows,

@@ -1,0 +1,419 @@
+// Explicit-system solves and the minimum-norm fallback (construct.py:123-165,198-210).
+//
+//  * dense_normal_kernel: one warp per problem, G = A^H A + lam R (R diagonal or
+//    full Hermitian) and rhs = A^H b formed in shared memory, complex Cholesky,
+//    two triangular solves, then the reference's acceptance test
+//    ||G x - rhs||_F <= 1e-8 ||rhs||_F (construct.py:146-152, 200-203).
+//  * minnorm_kernel: the reference's degenerate-case fallback
+//    `_stacked_lstsq` (construct.py:157-165): minimum-norm least squares of
+//    [A; Gamma] x = [b; 0] with Gamma^H Gamma = lam R, by a one-sided Jacobi SVD
+//    (fp64) of the real embedding of the stacked matrix, singular values below
+//    eps * max(M, N) * sigma_max dropped (numpy lstsq's rcond=None).
+//  * build_bins_kernel / scatter_bins_kernel: materialise A, b, reg of the bins
+//    K1 flagged during construction and write their re-solved layers back.
+#include "k1_solve.cuh"
+
+namespace fdl {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ inline double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+struct DenseParams {
+  int batch, m, n, C;
+  const double2* A;    // (batch, m, n)
+  const double2* b;    // (batch, m, C)
+  const double* reg;   // (batch, n) or nullptr
+  const double2* R;    // (batch, n, n) or nullptr
+  double lam;
+  double2* x;          // (batch, n, C)
+  signed char* status; // (batch): 0 ok, 2 needs the min-norm fallback, 3 singular at lam = 0
+};
+
+// complex helpers on double2
+__device__ inline double2 cm(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ inline double2 cjm(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+__global__ void dense_normal_kernel(DenseParams p) {
+  extern __shared__ double2 sh[];
+  const int prob = blockIdx.x, lane = threadIdx.x;
+  const int m = p.m, n = p.n, C = p.C;
+  double2* G = sh;              // n x n (full, Hermitian)
+  double2* G0 = G + n * n;      // copy for the residual
+  double2* Rh = G0 + n * n;     // n x C
+  double2* R0 = Rh + n * C;
+  const double2* A = p.A + (size_t)prob * m * n;
+  const double2* B = p.b + (size_t)prob * m * C;
+  for (int e = lane; e < n * n; e += 32) {
+    const int r = e / n, c = e % n;
+    double2 acc = make_double2(0, 0);
+    for (int j = 0; j < m; ++j) {
+      const double2 t = cjm(A[j * n + r], A[j * n + c]);
+      acc.x += t.x;
+      acc.y += t.y;
+    }
+    if (p.lam > 0.0) {
+      if (p.R) {
+        const double2 rv = p.R[((size_t)prob * n + r) * n + c];
+        acc.x += p.lam * rv.x;
+        acc.y += p.lam * rv.y;
+      } else if (p.reg && r == c) {
+        acc.x += p.lam * p.reg[(size_t)prob * n + r];
+      }
+    }
+    G[e] = acc;
+    G0[e] = acc;
+  }
+  for (int e = lane; e < n * C; e += 32) {
+    const int r = e / C, c = e % C;
+    double2 acc = make_double2(0, 0);
+    for (int j = 0; j < m; ++j) {
+      const double2 t = cjm(A[j * n + r], B[j * C + c]);
+      acc.x += t.x;
+      acc.y += t.y;
+    }
+    Rh[e] = acc;
+    R0[e] = acc;
+  }
+  __syncwarp();
+  // right-looking LDL^H (no square roots, like the reference's LU it only
+  // declares the system singular on an exactly zero pivot; the residual test
+  // below catches the rest), unit lower L stored below the diagonal, D on it
+  bool ok = true;
+  for (int k = 0; k < n; ++k) {
+    const double dk = G[k * n + k].x;
+    if (dk == 0.0 || !isfinite(dk)) {
+      ok = false;
+      break;
+    }
+    __syncwarp();
+    for (int e = lane; e < (n - k - 1) * (n - k - 1); e += 32) {
+      const int r = k + 1 + e / (n - k - 1), c = k + 1 + e % (n - k - 1);
+      if (c > r) continue;
+      const double2 vr = G[r * n + k], vc = G[c * n + k];
+      const double2 t = cm(vr, make_double2(vc.x, -vc.y));
+      G[r * n + c].x -= t.x / dk;
+      G[r * n + c].y -= t.y / dk;
+    }
+    __syncwarp();
+    for (int r = k + 1 + lane; r < n; r += 32) G[r * n + k] = make_double2(G[r * n + k].x / dk, G[r * n + k].y / dk);
+    __syncwarp();
+  }
+  double2* X = p.x + (size_t)prob * n * C;
+  if (ok && lane < C) {
+    const int c = lane;
+    for (int r = 0; r < n; ++r) {  // L z = rhs (unit lower)
+      double2 v = Rh[r * C + c];
+      for (int k = 0; k < r; ++k) {
+        const double2 t = cm(G[r * n + k], Rh[k * C + c]);
+        v.x -= t.x;
+        v.y -= t.y;
+      }
+      Rh[r * C + c] = v;
+    }
+    for (int r = 0; r < n; ++r) {  // D w = z
+      const double d = G[r * n + r].x;
+      Rh[r * C + c] = make_double2(Rh[r * C + c].x / d, Rh[r * C + c].y / d);
+    }
+    for (int r = n - 1; r >= 0; --r) {  // L^H x = w
+      double2 v = Rh[r * C + c];
+      for (int k = r + 1; k < n; ++k) {
+        const double2 t = cjm(G[k * n + r], Rh[k * C + c]);
+        v.x -= t.x;
+        v.y -= t.y;
+      }
+      Rh[r * C + c] = v;
+    }
+  }
+  __syncwarp();
+  // residual ||G0 x - rhs||_F <= 1e-8 ||rhs||_F  (construct.py:146-152)
+  double res = 0.0, ref = 0.0;
+  bool finite = true;
+  if (ok) {
+    for (int e = lane; e < n * C; e += 32) {
+      const int r = e / C, c = e % C;
+      double2 acc = make_double2(-R0[e].x, -R0[e].y);
+      for (int k = 0; k < n; ++k) {
+        const double2 t = cm(G0[r * n + k], Rh[k * C + c]);
+        acc.x += t.x;
+        acc.y += t.y;
+      }
+      res += acc.x * acc.x + acc.y * acc.y;
+      ref += R0[e].x * R0[e].x + R0[e].y * R0[e].y;
+      finite = finite && isfinite(Rh[e].x) && isfinite(Rh[e].y);
+    }
+  }
+  res = warp_sum(res);
+  ref = warp_sum(ref);
+  finite = __all_sync(FULL, finite);
+  const bool accept = ok && finite && sqrt(res) <= 1e-8 * fmax(sqrt(ref), 2.2250738585072014e-308);
+  for (int e = lane; e < n * C; e += 32) X[e] = Rh[e];
+  if (lane == 0) p.status[prob] = accept ? 0 : (p.lam == 0.0 ? 3 : 2);
+}
+
+// ---------------------------------------------------------------- min-norm
+struct MinNormParams {
+  int batch, m, n, C;
+  const double2* A;    // (batch, m, n)
+  const double2* b;    // (batch, m, C)
+  const double* reg;   // (batch, n) or nullptr (then R)
+  const double2* R;    // (batch, n, n)
+  double lam;
+  double2* x;          // (batch, n, C)
+  const signed char* status;  // only problems with status == 2 are solved (nullptr: all)
+  signed char* status_out;    // set to 0 on success, 1 on failure
+  double* scratch;     // per problem: S (Mr x Nr) + V (Nr x Nr) + Bt (Mr x C2) doubles
+};
+
+__global__ void minnorm_kernel(MinNormParams p) {
+  const int prob = blockIdx.x, lane = threadIdx.x;
+  if (p.status && p.status[prob] != 2) return;
+  const int m = p.m, n = p.n, C = p.C;
+  const int Mc = m + n, Mr = 2 * Mc, Nr = 2 * n;
+  double* S = p.scratch + (size_t)prob * ((size_t)Mr * Nr + (size_t)Nr * Nr + (size_t)Mr * C * 2);
+  double* V = S + (size_t)Mr * Nr;
+  double* Bt = V + (size_t)Nr * Nr;  // Mr x (2C): column 2c = embed(Re/Im part of b_c ...)
+  const double2* A = p.A + (size_t)prob * m * n;
+  const double2* B = p.b + (size_t)prob * m * C;
+  // stacked complex matrix Sc = [A; Gamma], Gamma^H Gamma = lam R
+  //   diagonal R: Gamma = diag(sqrt(lam reg)); full R: Gamma = sqrt(lam) L^H (R = L L^H)
+  // real embedding: S = [[Re Sc, -Im Sc], [Im Sc, Re Sc]] stored column-major
+  auto sc = [&](int row, int col) -> double2 {
+    if (row < m) return A[row * n + col];
+    const int k = row - m;
+    if (!p.R) {
+      return make_double2(k == col ? sqrt(p.lam * fmax(p.reg[(size_t)prob * n + k], 0.0)) : 0.0, 0.0);
+    }
+    return make_double2(0.0, 0.0);  // filled below for full R
+  };
+  for (int e = lane; e < Mc * n; e += 32) {
+    const int row = e / n, col = e % n;
+    const double2 v = sc(row, col);
+    S[(size_t)col * Mr + row] = v.x;
+    S[(size_t)(n + col) * Mr + row] = -v.y;
+    S[(size_t)col * Mr + Mc + row] = v.y;
+    S[(size_t)(n + col) * Mr + Mc + row] = v.x;
+  }
+  bool good = true;
+  if (p.R) {
+    // Cholesky of lam R (lane 0, small n), Gamma = L^H written into rows m..m+n-1
+    if (lane == 0) {
+      const double2* Rr = p.R + (size_t)prob * n * n;
+      // L in the V area (scratch), n x n complex = 2 n^2 doubles <= Nr^2
+      double2* L = reinterpret_cast<double2*>(V);
+      for (int i = 0; i < n * n; ++i) L[i] = make_double2(p.lam * Rr[i].x, p.lam * Rr[i].y);
+      for (int k = 0; k < n && good; ++k) {
+        double piv = L[k * n + k].x;
+        for (int s = 0; s < k; ++s) piv -= L[k * n + s].x * L[k * n + s].x + L[k * n + s].y * L[k * n + s].y;
+        if (!(piv > 0.0)) {
+          good = false;
+          break;
+        }
+        const double lkk = sqrt(piv);
+        L[k * n + k] = make_double2(lkk, 0.0);
+        for (int r = k + 1; r < n; ++r) {
+          double2 v = L[r * n + k];
+          for (int s = 0; s < k; ++s) {
+            const double2 t = cm(L[r * n + s], make_double2(L[k * n + s].x, -L[k * n + s].y));
+            v.x -= t.x;
+            v.y -= t.y;
+          }
+          L[r * n + k] = make_double2(v.x / lkk, v.y / lkk);
+        }
+      }
+      if (good) {
+        for (int k = 0; k < n; ++k)
+          for (int col = 0; col < n; ++col) {
+            // Gamma[k][col] = conj(L[col][k]) for col >= k, else 0
+            const double2 v = col >= k ? make_double2(L[col * n + k].x, -L[col * n + k].y) : make_double2(0.0, 0.0);
+            const int row = m + k;
+            S[(size_t)col * Mr + row] = v.x;
+            S[(size_t)(n + col) * Mr + row] = -v.y;
+            S[(size_t)col * Mr + Mc + row] = v.y;
+            S[(size_t)(n + col) * Mr + Mc + row] = v.x;
+          }
+      }
+    }
+    good = __shfl_sync(FULL, good, 0);
+  }
+  __syncwarp();
+  if (!good) {
+    if (lane == 0) p.status_out[prob] = 1;  // failed
+    return;
+  }
+  // embedded right-hand sides: for channel c, columns 2c (Re part) and 2c+1 (Im part)
+  for (int e = lane; e < Mc * C; e += 32) {
+    const int row = e / C, c = e % C;
+    const double2 v = row < m ? B[row * C + c] : make_double2(0.0, 0.0);
+    // complex b -> real [Re b; Im b]
+    Bt[(size_t)c * Mr + row] = v.x;
+    Bt[(size_t)c * Mr + Mc + row] = v.y;
+  }
+  for (int e = lane; e < Nr * Nr; e += 32) V[e] = (e / Nr == e % Nr) ? 1.0 : 0.0;
+  __syncwarp();
+  // one-sided Jacobi (Hestenes) on the columns of S
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int pc = 0; pc < Nr - 1; ++pc)
+      for (int qc = pc + 1; qc < Nr; ++qc) {
+        double al = 0, be = 0, ga = 0;
+        for (int i = lane; i < Mr; i += 32) {
+          const double sp = S[(size_t)pc * Mr + i], sq = S[(size_t)qc * Mr + i];
+          al += sp * sp;
+          be += sq * sq;
+          ga += sp * sq;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+        off = fmax(off, fabs(ga) / sqrt(al * be));
+        const double zeta = (be - al) / (2.0 * ga);
+        const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+        for (int i = lane; i < Mr; i += 32) {
+          const double sp = S[(size_t)pc * Mr + i], sq = S[(size_t)qc * Mr + i];
+          S[(size_t)pc * Mr + i] = cs * sp - sn * sq;
+          S[(size_t)qc * Mr + i] = sn * sp + cs * sq;
+        }
+        for (int i = lane; i < Nr; i += 32) {
+          const double vp = V[(size_t)pc * Nr + i], vq = V[(size_t)qc * Nr + i];
+          V[(size_t)pc * Nr + i] = cs * vp - sn * vq;
+          V[(size_t)qc * Nr + i] = sn * vp + cs * vq;
+        }
+        __syncwarp();
+      }
+    if (off < 1e-15) break;
+  }
+  // sigma_j = ||S_j||; x = sum_{sigma_j > cutoff} V_j (S_j^T b) / sigma_j^2
+  double smax = 0.0;
+  for (int j = 0; j < Nr; ++j) {
+    double s2 = 0;
+    for (int i = lane; i < Mr; i += 32) s2 += S[(size_t)j * Mr + i] * S[(size_t)j * Mr + i];
+    smax = fmax(smax, sqrt(warp_sum(s2)));
+  }
+  const double cutoff = 2.220446049250313e-16 * (double)(Mc > n ? Mc : n) * smax;
+  double2* X = p.x + (size_t)prob * n * C;
+  for (int c = 0; c < C; ++c) {
+    double xr[4] = {0.0, 0.0, 0.0, 0.0};  // rows lane + 32 i of x~ (Nr <= 128)
+    for (int j = 0; j < Nr; ++j) {
+      double s2 = 0, proj = 0;
+      for (int i = lane; i < Mr; i += 32) {
+        const double sv = S[(size_t)j * Mr + i];
+        s2 += sv * sv;
+        proj += sv * Bt[(size_t)c * Mr + i];
+      }
+      s2 = warp_sum(s2);
+      proj = warp_sum(proj);
+      const double w = (sqrt(s2) > cutoff) ? proj / s2 : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = lane + 32 * i;
+        if (row < Nr) xr[i] += V[(size_t)j * Nr + row] * w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = lane + 32 * i;
+      if (row < Nr) {
+        if (row < n) X[(size_t)row * C + c].x = xr[i];  // x~ = [Re x; Im x]
+        else X[(size_t)(row - n) * C + c].y = xr[i];
+      }
+    }
+  }
+  if (lane == 0) p.status_out[prob] = 2;  // solved by the minimum-norm fallback
+}
+
+// ---------------------------------------------------------------- construction bins
+__global__ void build_bins_kernel(SolveParams p, const int* bins, int nb, double2* A, double2* b, double* reg) {
+  const int t = blockIdx.x;
+  if (t >= nb) return;
+  const long long bin = bins[t];
+  const int i = (int)(bin / p.Whp), kx = (int)(bin % p.Whp);
+  const int ky = p.rows[i];
+  const double ox = omega_x_label(kx, p.Wp), oy = omega_y_label(ky, p.Hp);
+  const bool nyq_x = (p.Wp % 2 == 0) && kx == p.Wp / 2;
+  const bool nyq_y = (p.Hp % 2 == 0) && ky == p.Hp / 2;
+  const size_t plane = (size_t)p.nrows * p.Whp;
+  for (int e = threadIdx.x; e < p.m * p.n; e += blockDim.x) {
+    const int j = e / p.n, k = e % p.n;
+    const cd a = system_entry(p, j, k, kx, ky, ox, oy, nyq_x, nyq_y);
+    A[(size_t)t * p.m * p.n + e] = make_double2(a.re, a.im);
+  }
+  for (int e = threadIdx.x; e < p.m * p.C; e += blockDim.x) {
+    const int j = e / p.C, c = e % p.C;
+    const float2 v = p.spectra[((size_t)j * p.C + c) * plane + (size_t)i * p.Whp + kx];
+    b[(size_t)t * p.m * p.C + e] = make_double2(v.x, v.y);
+  }
+  const double osq = ox * ox + oy * oy;
+  for (int k = threadIdx.x; k < p.n; k += blockDim.x) reg[(size_t)t * p.n + k] = osq * osq * p.d4[k] + p.eps;
+}
+
+__global__ void scatter_bins_kernel(SolveParams p, const int* bins, int nb, const double2* x,
+                                    const signed char* st) {
+  const int t = blockIdx.x;
+  if (t >= nb) return;
+  const long long bin = bins[t];
+  const int i = (int)(bin / p.Whp), kx = (int)(bin % p.Whp);
+  const size_t plane = (size_t)p.nrows * p.Whp;
+  for (int e = threadIdx.x; e < p.n * p.C; e += blockDim.x) {
+    const int k = e / p.C, c = e % p.C;
+    const double2 v = x[(size_t)t * p.n * p.C + e];
+    p.layers[((size_t)k * p.C + c) * plane + (size_t)i * p.Whp + kx] = make_float2((float)v.x, (float)v.y);
+  }
+  if (threadIdx.x == 0 && p.status) p.status[bin] = st[t] == 2 ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
+}
+
+}  // namespace
+
+size_t dense_scratch_doubles(int m, int n, int C) {
+  const size_t Mr = 2 * (size_t)(m + n), Nr = 2 * (size_t)n;
+  return Mr * Nr + Nr * Nr + Mr * C * 2;
+}
+
+int dense_solve_launch(int batch, int m, int n, int C, const double2* A, const double2* b, const double* reg,
+                       const double2* R, double lam, double2* x, signed char* status, signed char* status2,
+                       double* scratch, bool force_minnorm, cudaStream_t st) {
+  if (batch == 0) return FDL_OK;
+  if (n > 64) return fail(FDL_ERR_UNSUPPORTED, "dense solve supports n <= 64");
+  if (!force_minnorm) {
+    DenseParams dp{batch, m, n, C, A, b, reg, R, lam, x, status};
+    const size_t smem = sizeof(double2) * (2 * (size_t)n * n + 2 * (size_t)n * C);
+    if (smem > 200 * 1024) return fail(FDL_ERR_UNSUPPORTED, "dense solve: system too large");
+    FDL_CUDA_CHECK(cudaFuncSetAttribute(dense_normal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dense_normal_kernel<<<batch, 32, smem, st>>>(dp);
+    FDL_LAUNCH_CHECK("dense_normal_kernel");
+  } else {
+    FDL_CUDA_CHECK(cudaMemsetAsync(status, 2, batch, st));
+  }
+  if (lam <= 0.0) return FDL_OK;  // lam = 0: no fallback (the reference raises RankDeficiencyError)
+  MinNormParams mp{batch, m, n, C, A, b, reg, R, lam, x, status, status2 ? status2 : status, scratch};
+  minnorm_kernel<<<batch, 32, 0, st>>>(mp);
+  FDL_LAUNCH_CHECK("minnorm_kernel");
+  return FDL_OK;
+}
+
+int build_bins_launch(const SolveParams& p, const int* bins, int nb, double2* A, double2* b, double* reg,
+                      cudaStream_t st) {
+  if (nb == 0) return FDL_OK;
+  build_bins_kernel<<<nb, 128, 0, st>>>(p, bins, nb, A, b, reg);
+  FDL_LAUNCH_CHECK("build_bins_kernel");
+  return FDL_OK;
+}
+
+int scatter_bins_launch(const SolveParams& p, const int* bins, int nb, const double2* x, const signed char* st2,
+                        cudaStream_t st) {
+  if (nb == 0) return FDL_OK;
+  scatter_bins_kernel<<<nb, 128, 0, st>>>(p, bins, nb, x, st2);
+  FDL_LAUNCH_CHECK("scatter_bins_kernel");
+  return FDL_OK;
+}
+
+}  // namespace fdl
