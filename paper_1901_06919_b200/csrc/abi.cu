@@ -112,7 +112,7 @@ struct SolvePlan {
   size_t extra = 0;  // device-only scratch after the uploaded block (not copied)
   size_t ws_bytes() const { return blob.size() + align256(extra); }
   bool has_axes = false;
-  std::vector<size_t> o_tab_re, o_tab_im;
+  std::vector<size_t> o_tab_re, o_tab_im, o_quad;
 };
 
 bool finite_all(const double* x, size_t n) {
@@ -261,6 +261,21 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
     if (ap.rows < 2 || ap.cols < 2 || !ap.table_re) return fail(FDL_ERR_INVALID, "aperture table needs >= 2x2 entries");
     P.o_tab_re.push_back(B.add(ap.table_re, sizeof(double) * ap.rows * ap.cols));
     P.o_tab_im.push_back(ap.table_im ? B.add(ap.table_im, sizeof(double) * ap.rows * ap.cols) : (size_t)-1);
+    if (!ap.table_im && mode == MODE_REALA) {
+      const size_t R = ap.rows, Cc = ap.cols;
+      std::vector<double> quad(4 * (R * Cc + 1), 0.0);
+      for (size_t iy = 0; iy + 1 < R; ++iy)
+        for (size_t ix = 0; ix + 1 < Cc; ++ix) {
+          double* e = &quad[4 * (iy * Cc + ix)];
+          e[0] = ap.table_re[iy * Cc + ix];
+          e[1] = ap.table_re[iy * Cc + ix + 1];
+          e[2] = ap.table_re[(iy + 1) * Cc + ix];
+          e[3] = ap.table_re[(iy + 1) * Cc + ix + 1];
+        }
+      P.o_quad.push_back(B.add(quad.data(), quad.size() * sizeof(double)));
+    } else {
+      P.o_quad.push_back((size_t)-1);
+    }
   }
   P.o_cnt = B.reserve(sizeof(unsigned long long));
   if (factored) {
@@ -334,6 +349,8 @@ void bind_solve(SolvePlan& P, const fdl_solve_desc* D, void* ws) {
     da.step_x = ap.step_x;
     da.xi0_y = ap.xi0_y;
     da.step_y = ap.step_y;
+    da.quad = P.o_quad[a] == (size_t)-1 ? nullptr : at<double2>(ws, P.o_quad[a]);
+    da.inv_step_x = 1.0 / ap.step_x;
     host_aps[a] = da;
   }
 }

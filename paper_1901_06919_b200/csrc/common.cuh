@@ -57,6 +57,10 @@ struct DevAperture {
   const double* re;
   const double* im;  // nullptr for a real table
   double xi0_x, step_x, xi0_y, step_y;
+  // fast path (real tables, construction K1 mode 2): "quad" table, entry (iy, ix)
+  // = {(T[iy][ix], T[iy][ix+1]), (T[iy+1][ix], T[iy+1][ix+1])}, entry rows*cols = 0
+  const double2* quad;
+  double inv_step_x;
 };
 
 // Bilinear axis lookup of ApertureSpec._axis_lookup (lfmodel.py:72-79):

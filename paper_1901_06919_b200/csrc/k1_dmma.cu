@@ -87,6 +87,12 @@ struct FastParams {
 
 __host__ __device__ constexpr int blk(int I, int J) { return I * (I + 1) / 2 + J; }
 
+// mode 2: per-(view, layer) half of the aperture lookup, shared by a CTA's row of bins
+struct YEntry {
+  double t, fy;
+  int iyoff, ai;
+};
+
 // Per-axis phase tables of mode 1, once per column / row of the slab (the
 // reference's `_phase_tables`, construct.py:68-80, restricted to the distinct
 // u and v values and the first half of the layers).
@@ -114,7 +120,7 @@ __global__ void k1_axis_tables_kernel(SolveParams p, FastParams f) {
 }
 
 template <int NB, int MODE, int ODD>
-__global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 4 ? 2 : 1))) k1_fast_kernel(SolveParams p, FastParams f) {
+__global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1))) k1_fast_kernel(SolveParams p, FastParams f) {
   constexpr int NBc = (NB - ODD) / 2;  // blocks of the cos half (= of the sin half), mode 1
   constexpr int NBLK = NB * (NB + 1) / 2;
   constexpr int NP = NB * 8;
@@ -132,8 +138,9 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 4 ? 2 : 1)))
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hw : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hw : 0;
   const int m4 = (p.m + 3) & ~3;
-  const int ro_words = (MODE == MODE_SYMREAL) ? m4 : 0;  // int2 per view = one double word
+  const int ro_words = (MODE == MODE_SYMREAL) ? m4 : 3 * p.m * p.n;  // mode 2: YEntry per (view, layer)
   int2* ROWOFF = reinterpret_cast<int2*>(PY + py_words);
+  YEntry* YT = reinterpret_cast<YEntry*>(PY + py_words);
   const int bs_words = (p.m * p.C + 1) & ~1;  // staged spectra, one float2 per (view, channel); keeps 16-B alignment
   const int per_warp = px_words + 64 + 64 + NB * 64 + NP * 8 + bs_words;
   double* base = smem + py_words + ro_words + warp * per_warp;
@@ -149,6 +156,28 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 4 ? 2 : 1)))
     for (int e = threadIdx.x; e < f.nv * f.hw; e += blockDim.x) reinterpret_cast<double2*>(PY)[e] = src[e];
     for (int e = threadIdx.x; e < m4; e += blockDim.x)
       ROWOFF[e] = e < p.m ? make_int2(f.u_idx[e] * f.hw, f.v_idx[e] * f.hw) : make_int2(0, 0);
+  } else {
+    // mode 2: the y half of every bilinear lookup depends only on (view, layer, row):
+    // t_jk = scale_j (s_j - d_k), (iy, fy) of t_jk wy -- shared by the CTA's bins
+    for (int e = threadIdx.x; e < p.m * p.n; e += blockDim.x) {
+      const int j = e / p.n, k = e % p.n;
+      const int ai = p.view_ap ? p.view_ap[j] : -1;
+      YEntry ye;
+      ye.ai = ai;
+      ye.t = 0.0;
+      ye.fy = 0.0;
+      ye.iyoff = 0;
+      if (ai >= 0) {
+        const DevAperture& ap = p.aps[ai];
+        ye.t = __dmul_rn(p.scale[j], __dsub_rn(p.s[j], p.d[k]));
+        int iy;
+        double fy;
+        const bool ok = axis_lookup(__dmul_rn(ye.t, oy), ap.xi0_y, ap.step_y, ap.rows, iy, fy);
+        ye.fy = fy;
+        ye.iyoff = ok ? iy * ap.cols : ap.rows * ap.cols;  // the quad table's zero entry
+      }
+      YT[e] = ye;
+    }
   }
   __syncthreads();
   if (kx >= p.Whp) return;  // warp-uniform; no block barriers below
@@ -226,16 +255,31 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 4 ? 2 : 1)))
       }
     } else {  // MODE_REALA: A_jk = psi_j(t_jk wx, t_jk wy) (all shifts are zero)
       if (!valid) bf = 0.0;
-      const int ai = (valid && p.view_ap) ? p.view_ap[j] : -1;
 #pragma unroll
       for (int I = 0; I < NB; ++I) {
         const int k = I * 8 + q;
         if (valid && k < p.n) {
-          if (ai < 0) {
+          const YEntry ye = YT[j * p.n + k];
+          if (ye.ai < 0) {
             mf[I] = 1.0;
           } else {
-            const double tt = __dmul_rn(p.scale[j], __dsub_rn(p.s[j], p.d[k]));
-            mf[I] = aperture_eval(p.aps[ai], __dmul_rn(tt, ox), __dmul_rn(tt, oy)).re;
+            const DevAperture& ap = p.aps[ye.ai];
+            if (ap.quad) {
+              // x half of the bilinear lookup (lfmodel.py:72-99) + one 32-byte quad-table read
+              const double pos = (__dmul_rn(ye.t, ox) - ap.xi0_x) * ap.inv_step_x;
+              const bool okx = (pos >= 0.0) && (pos <= (double)(ap.cols - 1));
+              // inside the table pos >= 0, so truncation is floor; the clip to cols-2
+              // only bites at pos == cols-1 (then fx = 1) -- no fp64 min/max needed
+              const int ix = okx ? min((int)pos, ap.cols - 2) : 0;
+              const double fx = pos - (double)ix;
+              const int zero = ap.rows * ap.cols;
+              const int qi = okx ? min(ye.iyoff + ix, zero) : zero;
+              const double2 top = ap.quad[2 * qi], bot = ap.quad[2 * qi + 1];
+              const double gy = 1.0 - ye.fy, gx = 1.0 - fx;
+              mf[I] = (top.x * gy) * gx + (top.y * gy) * fx + (bot.x * ye.fy) * gx + (bot.y * ye.fy) * fx;
+            } else {
+              mf[I] = aperture_eval(ap, __dmul_rn(ye.t, ox), __dmul_rn(ye.t, oy)).re;
+            }
           }
         }
       }
@@ -506,7 +550,7 @@ template <int NB, int MODE, int ODD>
 int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hw : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hw : 0;
-  const int ro_words = (MODE == MODE_SYMREAL) ? ((p.m + 3) & ~3) : 0;
+  const int ro_words = (MODE == MODE_SYMREAL) ? ((p.m + 3) & ~3) : 3 * p.m * p.n;
   const size_t smem = sizeof(double) * ((size_t)py_words + ro_words +
                                         (size_t)WARPS * (px_words + 128 + NB * 64 + NB * 64 + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
   if (smem > 220 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
