@@ -235,6 +235,8 @@ def run_ours(args, rank, world, device):
             return fdl.FdlModel(disparities=d, layers=full, grid=fdl.FrequencyGrid(Wp, Hp), width=W, height=H,
                                 pad_margin=pad), 1
         spectra, sumsq = K.views_to_spectra(views, pad)
+        if ev is not None:
+            ev[2].record(stream)  # K0 done (pack + cuFFT R2C + sum|b|^2)
         lam = K.lambda_from_sumsq(sumsq.cpu().numpy(), Q, m)
         if ev is not None:
             ev[0].record(stream)
@@ -246,10 +248,10 @@ def run_ours(args, rank, world, device):
         return fdl.FdlModel(disparities=d, layers=layers, grid=fdl.FrequencyGrid(Wp, Hp), width=W, height=H,
                             pad_margin=pad), path
 
-    def render_step(model):
+    def render_step(model, timing=None):
         if sharded:
-            return R.render_many_device(model, my_reqs, batch=args.batch) if my_reqs else None
-        return R.render_many_device(model, reqs, batch=args.batch)
+            return R.render_many_device(model, my_reqs, batch=args.batch, timing=timing) if my_reqs else None
+        return R.render_many_device(model, reqs, batch=args.batch, timing=timing)
 
     for _ in range(args.warmup):
         model, path = construct_step()
@@ -261,13 +263,14 @@ def run_ours(args, rank, world, device):
     sampler = ClockSampler(device.index if device.index is not None else 0)
     sampler.start()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ isolates the step's launches
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    rtim = []
     for s in range(args.steps):
         e = evs[s]
         e[0].record(stream)
-        model, path = construct_step(ev=(e[3], e[4]))
+        model, path = construct_step(ev=(e[3], e[4], e[5]))
         e[1].record(stream)
-        render_step(model)
+        render_step(model, timing=rtim)
         e[2].record(stream)
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
@@ -278,6 +281,14 @@ def run_ours(args, rank, world, device):
     t_con = np.array([e[0].elapsed_time(e[1]) for e in evs]) / 1e3
     t_ren = np.array([e[1].elapsed_time(e[2]) for e in evs]) / 1e3
     t_k1 = np.array([e[3].elapsed_time(e[4]) for e in evs]) / 1e3
+    stages = {}
+    if not sharded:
+        stages["k0_pack_fft_sumsq_ms"] = float(np.mean([e[0].elapsed_time(e[5]) for e in evs]))
+        stages["k1_ms"] = float(np.mean(t_k1)) * 1e3
+        stages["k2_symmetrize_ms"] = float(np.mean([e[4].elapsed_time(e[1]) for e in evs]))
+    if rtim:
+        stages["k3_render_spectra_ms"] = float(sum(t[0].elapsed_time(t[1]) for t in rtim)) / args.steps
+        stages["k4_c2r_crop_ms"] = float(sum(t[1].elapsed_time(t[2]) for t in rtim)) / args.steps
     tot = np.array([t_con.sum(), t_ren.sum(), t_k1.sum()])
     if world > 1:
         tt = torch.tensor(tot, device=device)
@@ -314,6 +325,7 @@ def run_ours(args, rank, world, device):
                    "k1_path": int(path)},
         "render": {"value": V / t_ren_mean, "unit": "views/s", "ms": 1e3 * t_ren_mean},
         "construct_ms": 1e3 * t_con_mean,
+        "stages_ms": stages,
         "k1_ms": 1e3 * t_k1_mean,
         "roofline": {"bound": "tensor", "kernel": "k1_fast_kernel (fp64 DMMA)",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",

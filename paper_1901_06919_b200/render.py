@@ -241,7 +241,7 @@ def _check_gamma(model: FdlModel, req: RenderRequest):
                          f"(model stores {model.color_space!r} data)")
 
 
-def render_many_device(model: FdlModel, reqs, batch: int = 64):
+def render_many_device(model: FdlModel, reqs, batch: int = 64, timing=None):
     """Render requests to a (V, H, W, C) float32 CUDA tensor (cropped per req.crop,
     which must agree across the batch) plus per-view OOB counts.  Device-resident
     form of `render_many`; no host round trip besides the OOB counts."""
@@ -283,8 +283,14 @@ def render_many_device(model: FdlModel, reqs, batch: int = 64):
                     aps.append(r.aperture)
                     view_ap[i] = len(aps) - 1
                 t[i] = r.f * (r.s - d)
+        evs = None
+        if timing is not None:
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            evs[0].record()
         spec = render_spectra_batch(layers, d, Hp, Wp, pu, pv, t=t,
                                     view_ap=view_ap if aps else None, apertures=aps, oob=oob[b0:b0 + V])
+        if evs is not None:
+            evs[1].record()
         flags = srgb[b0:b0 + V]
         if all(flags) or not any(flags):
             out[b0:b0 + V] = spectra_to_images(spec, Hp, Wp, pad, Ho, Wo, srgb=flags[0])
@@ -292,6 +298,9 @@ def render_many_device(model: FdlModel, reqs, batch: int = 64):
             for i in range(V):
                 out[b0 + i:b0 + i + 1] = spectra_to_images(spec[i:i + 1].contiguous(), Hp, Wp, pad, Ho, Wo,
                                                            srgb=flags[i])
+        if evs is not None:
+            evs[2].record()
+            timing.append(evs)
     return out, oob
 
 
