@@ -378,10 +378,10 @@ def run_e2e(args, case, dims, device):
     h2d = int(host_views.numel() * 4)
     d2h = int(out_host.numel() * 8)
     return {"value": Q * n / float(np.mean(tc)), "unit": "freq·layers/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h + V * H * W * C * 4,
+            "d2h_bytes_per_step": d2h + V * H * W * C * 8,
             "construct_ms": 1e3 * float(np.mean(tc)),
             "render": {"value": V / float(np.mean(tr)), "unit": "views/s", "ms": 1e3 * float(np.mean(tr)),
-                       "d2h_bytes_per_step": V * H * W * C * 4}}
+                       "d2h_bytes_per_step": V * H * W * C * 8}}  # float64 images, like the reference
 
 
 # ----------------------------------------------------------------------------- CPU (oracle) arm

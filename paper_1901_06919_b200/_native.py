@@ -186,3 +186,20 @@ def stream_handle(device=None):
 def workspace(nbytes: int, device):
     import torch
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+_copy_streams = threading.local()
+
+
+def copy_stream(device):
+    """A per-thread, per-device side stream for host<->device copies that overlap
+    the kernels on the current stream."""
+    import torch
+    cache = getattr(_copy_streams, "by_dev", None)
+    if cache is None:
+        cache = _copy_streams.by_dev = {}
+    key = torch.device(device).index
+    s = cache.get(key)
+    if s is None:
+        s = cache[key] = torch.cuda.Stream(device=device)
+    return s

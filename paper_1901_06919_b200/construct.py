@@ -301,6 +301,61 @@ def views_to_spectra(views_dev, pad):
     return spectra, sumsq
 
 
+UPLOAD_CHUNK_BYTES = 24 << 20
+
+
+def views_to_spectra_host(images, pad, device, chunk_bytes: int = UPLOAD_CHUNK_BYTES):
+    """K0 on HOST views with the upload overlapped: view chunks go host->device
+    on a side stream while K0 transforms the previous chunk on the current
+    stream.  Pinned torch input is copied directly; anything else passes
+    through a two-slot pinned staging ring.  K0 is batch-independent bit for
+    bit (tests/test_gpu_sharded.py), so the result equals the one-shot call."""
+    import torch
+    src = images if _is_torch(images) else torch.from_numpy(np.ascontiguousarray(images, dtype=np.float32))
+    if src.dtype != torch.float32 or not src.is_contiguous():
+        src = src.to(torch.float32).contiguous()
+    m, H, W, C = src.shape
+    Hp, Wp = H + 2 * pad, W + 2 * pad
+    per = max(1, min(m, chunk_bytes // max(1, H * W * C * 4)))
+    spectra = torch.empty((m, C, Hp, Wp // 2 + 1), dtype=torch.complex64, device=device)
+    sumsq = torch.empty((m,), dtype=torch.float64, device=device)
+    views_dev = torch.empty((m, H, W, C), dtype=torch.float32, device=device)
+    L = nat.lib()
+    ws_bytes = L.fdl_views_to_spectra_workspace(per, H, W, C, pad)
+    if ws_bytes == 0:
+        raise nat.FdlNativeError("fdl_views_to_spectra_workspace: " + L.fdl_last_error().decode())
+    ws = nat.workspace(ws_bytes, device)
+    compute = torch.cuda.current_stream(device)
+    copy = nat.copy_stream(device)
+    copy.wait_stream(compute)  # views_dev was allocated on the compute stream
+    pinned = src.is_pinned()
+    ring = [] if pinned else [torch.empty((per, H, W, C), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    ring_ev = [None, None]
+    for i, j0 in enumerate(range(0, m, per)):
+        j1 = min(m, j0 + per)
+        with torch.cuda.stream(copy):
+            if pinned:
+                views_dev[j0:j1].copy_(src[j0:j1], non_blocking=True)
+            else:
+                b = i % 2
+                if ring_ev[b] is not None:
+                    ring_ev[b].synchronize()  # the slot's previous H2D has drained
+                ring[b][:j1 - j0].copy_(src[j0:j1])
+                views_dev[j0:j1].copy_(ring[b][:j1 - j0], non_blocking=True)
+                ring_ev[b] = torch.cuda.Event()
+                ring_ev[b].record(copy)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        compute.wait_event(ev)
+        nat.check(L.fdl_views_to_spectra(views_dev[j0].data_ptr(), j1 - j0, H, W, C, pad,
+                                         spectra[j0].data_ptr(), sumsq[j0:].data_ptr(), ws.data_ptr(),
+                                         ws.numel(), nat.stream_handle(device)), "fdl_views_to_spectra")
+    for e in ring_ev:
+        if e is not None:
+            e.synchronize()  # the staging ring may be reused by the caching host allocator
+    return spectra, sumsq
+
+
 def symmetrize(layers, Hp, Wp, rows=None, mirror=None):
     n, C, nrows, _ = layers.shape
     L = nat.lib()
@@ -359,9 +414,10 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
     H, W, C = views.height, views.width, views.channels
     Hp, Wp = H + 2 * pad_margin, W + 2 * pad_margin
     grid = FrequencyGrid(width=Wp, height=Hp)
-    views_dev = _views_device(views.images, dev)
-    spectra, sumsq = views_to_spectra(views_dev, pad_margin)
-    del views_dev
+    if _is_torch(views.images) and views.images.is_cuda:
+        spectra, sumsq = views_to_spectra(_views_device(views.images, dev), pad_margin)
+    else:
+        spectra, sumsq = views_to_spectra_host(views.images, pad_margin, dev)
     if lam is None:
         lam = lambda_from_sumsq(sumsq.cpu().numpy(), grid.num_entries, m)
     if lam < 0:

@@ -241,7 +241,7 @@ def _check_gamma(model: FdlModel, req: RenderRequest):
                          f"(model stores {model.color_space!r} data)")
 
 
-def render_many_device(model: FdlModel, reqs, batch: int = 64, timing=None):
+def render_many_device(model: FdlModel, reqs, batch: int = 64, timing=None, on_batch=None):
     """Render requests to a (V, H, W, C) float32 CUDA tensor (cropped per req.crop,
     which must agree across the batch) plus per-view OOB counts.  Device-resident
     form of `render_many`; no host round trip besides the OOB counts."""
@@ -301,6 +301,8 @@ def render_many_device(model: FdlModel, reqs, batch: int = 64, timing=None):
         if evs is not None:
             evs[2].record()
             timing.append(evs)
+        if on_batch is not None:
+            on_batch(b0, V, out[b0:b0 + V])
     return out, oob
 
 
@@ -325,8 +327,30 @@ def render_many(model: FdlModel, reqs, batch: int = 64, dtype=np.float64) -> lis
     float32 with dtype=np.float32); stats describe the last request."""
     t0 = time.perf_counter()
     reqs = list(reqs)
-    imgs, oob = render_many_device(model, reqs, batch)
-    host = _to_numpy_images(imgs, dtype)
+    import torch
+    tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+    host_t, copy = None, None
+
+    def drain(b0, V, dev_imgs):
+        # cast this batch on the compute stream, read it back on the copy
+        # stream while the next batch renders
+        nonlocal host_t, copy
+        if host_t is None:
+            host_t = torch.empty((len(reqs),) + tuple(dev_imgs.shape[1:]), dtype=tdt, pin_memory=True)
+            copy = nat.copy_stream(dev_imgs.device)
+        cast = dev_imgs.to(tdt)
+        ev = torch.cuda.Event()
+        ev.record()
+        copy.wait_event(ev)
+        with torch.cuda.stream(copy):
+            host_t[b0:b0 + V].copy_(cast, non_blocking=True)
+        cast.record_stream(copy)
+
+    _, oob = render_many_device(model, reqs, batch, on_batch=drain)
+    copy.synchronize()
+    host = host_t.numpy()
+    if host.shape[-1] == 1:
+        host = host[..., 0]
     oob_h = oob.cpu().numpy()
     for r, cnt in zip(reqs, oob_h):
         if _uses_aperture(r):
