@@ -14,6 +14,15 @@
 
 namespace fdl {
 
+// k0_fft.cu: the shared-memory FFT engine path
+bool fft_engine_applies(int Hp, int Wp, int C);
+size_t engine_fwd_ws(int m, int H, int W, int C, int pad);
+int engine_fwd(const float* views, int m, int H, int W, int C, int pad, float2* spectra, double* view_sumsq,
+               void* ws, cudaStream_t st);
+size_t engine_inv_ws(int V, int C, int Hp, int Wp);
+int engine_inv(const float2* spectra, int V, int C, int Hp, int Wp, int pad, int Ho, int Wo, int srgb, float* images,
+               void* ws, cudaStream_t st);
+
 namespace {
 
 struct PlanKey {
@@ -218,6 +227,10 @@ inline int grid_for(size_t total, int threads) {
 
 int views_to_spectra_ws(int m, int H, int W, int C, int pad, size_t* bytes) {
   const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+  if (fft_engine_applies(Hp, Wp, C)) {
+    *bytes = engine_fwd_ws(m, H, W, C, pad);
+    return FDL_OK;
+  }
   Plan* plan;
   int rc = get_plan(Hp, Wp, m * C, 0, &plan);
   if (rc) return rc;
@@ -233,6 +246,8 @@ int views_to_spectra(const float* views, int m, int H, int W, int C, int pad, fd
   int rc = views_to_spectra_ws(m, H, W, C, pad, &need);
   if (rc) return rc;
   if (ws_bytes < need || (need && !ws)) return fail(FDL_ERR_INVALID, "workspace too small for fdl_views_to_spectra");
+  if (fft_engine_applies(Hp, Wp, C))
+    return engine_fwd(views, m, H, W, C, pad, reinterpret_cast<float2*>(spectra), view_sumsq, ws, st);
   Plan* plan;
   get_plan(Hp, Wp, m * C, 0, &plan);
   float* padded = reinterpret_cast<float*>(ws);
@@ -272,6 +287,10 @@ int gather_rows(const fdl_c64* src, int m, int C, int Hp, int Whp, const int* ro
 }
 
 int spectra_to_images_ws(int V, int C, int Hp, int Wp, size_t* bytes) {
+  if (fft_engine_applies(Hp, Wp, C)) {
+    *bytes = engine_inv_ws(V, C, Hp, Wp);
+    return FDL_OK;
+  }
   Plan* plan;
   int rc = get_plan(Hp, Wp, V * C, 1, &plan);
   if (rc) return rc;
@@ -286,6 +305,8 @@ int spectra_to_images(fdl_c64* spectra, int V, int C, int Hp, int Wp, int pad, i
   if (rc) return rc;
   if (ws_bytes < need || !ws) return fail(FDL_ERR_INVALID, "workspace too small for fdl_spectra_to_images");
   if (pad < 0 || Ho + pad > Hp || Wo + pad > Wp) return fail(FDL_ERR_INVALID, "crop window outside the grid");
+  if (fft_engine_applies(Hp, Wp, C))
+    return engine_inv(reinterpret_cast<const float2*>(spectra), V, C, Hp, Wp, pad, Ho, Wo, srgb, images, ws, st);
   Plan* plan;
   get_plan(Hp, Wp, V * C, 1, &plan);
   float* planes = reinterpret_cast<float*>(ws);
