@@ -24,7 +24,13 @@ namespace fft {
 constexpr int KOUT = 12;        // output pairs per stage-1 work item
 // CTA size cap per power-of-two factor: stage 2 keeps 2M floats live per
 // thread, so larger M needs more registers per thread (no spills at these caps)
+// Rows kernels: 288 threads, 2 CTAs/SM; cols kernels: 192 threads, 3 CTAs/SM
+// (register caps 113 / 113); M >= 16: one 384-thread CTA per SM.
 __host__ __device__ constexpr int max_threads(int M) { return M >= 16 ? 384 : 320; }
+__host__ __device__ constexpr int rows_threads(int M) { return M >= 16 ? 384 : 288; }
+__host__ __device__ constexpr int rows_blocks(int M) { return M >= 16 ? 1 : 2; }
+__host__ __device__ constexpr int cols_threads(int M) { return M >= 16 ? 384 : 192; }
+__host__ __device__ constexpr int cols_blocks(int M) { return M >= 16 ? 1 : 3; }
 
 // n / d for 0 <= n < 2^31 by multiply-high (round-up method): 3 instructions
 // instead of the ~20 of a runtime 32-bit division.
@@ -84,6 +90,86 @@ __host__ inline Geo make_geo(int N, int B) {
 }
 
 __host__ inline int threads_for(const Geo& g) { return g.B * g.M * g.G; }
+
+// Shared-memory wavefronts of one warp's 8-byte accesses (bank = word % 32;
+// a bank serves one distinct word per wavefront).
+__host__ inline int warp_wavefronts(const int* slots) {
+  int best = 0;
+  for (int bank = 0; bank < 32; ++bank) {
+    int words[64], nw = 0;
+    for (int l = 0; l < 32; ++l)
+      for (int h = 0; h < 2; ++h) {
+        const int w = 2 * slots[l] + h;
+        if (w % 32 != bank) continue;
+        bool seen = false;
+        for (int i = 0; i < nw; ++i) seen |= words[i] == w;
+        if (!seen) words[nw++] = w;
+      }
+    best = nw > best ? nw : best;
+  }
+  return best;
+}
+
+// Pick the slot strides (SC, SR) that minimise bank conflicts over the
+// kernels' access patterns (lane -> slot maps of the loads, both stages and
+// the stores; rows = the row kernels' column-owning threads, else the column
+// kernels' (b, row) threads).
+__host__ inline void tune_strides(Geo& g, bool rows, int threads) {
+  const int B = g.B, M = g.M, P = g.P;
+  const int warps = (threads + 31) / 32;
+  long best_cost = -1;
+  int bsc = g.SC, bsr = g.SR;
+  for (int sc = B; sc <= B + 8; ++sc) {
+    for (int sr = M * sc; sr <= M * sc + 15; ++sr) {
+      if (M == 1 && sr != sc * M && sr > sc + 15) break;
+      auto sin = [&](int n) { return (n / M) * sr + (n % M) * sc; };
+      auto sout = [&](int k) { return (k % P) * sr + (k / P) * sc; };
+      long cost = 0;
+      int sl[32];
+      for (int w = 0; w < warps; ++w) {
+        for (int l = 0; l < 32; ++l) {  // stage 1 reads (and per-j strides)
+          const int t = 32 * w + l;
+          sl[l] = (t / B % M) * sc + t % B + 3 * sr;
+        }
+        cost += 2 * warp_wavefronts(sl);
+        for (int l = 0; l < 32; ++l) {  // stage 1 writes
+          const int t = 32 * w + l;
+          sl[l] = (t / (B * M) * KOUT + 1) * sr + (t / B % M) * sc + t % B;
+        }
+        cost += warp_wavefronts(sl);
+        for (int l = 0; l < 32; ++l) {  // stage 2
+          const int t = 32 * w + l;
+          sl[l] = (t / B % P) * sr + 1 * sc + t % B;
+        }
+        cost += warp_wavefronts(sl);
+        if (rows) {
+          for (int l = 0; l < 32; ++l) sl[l] = sin((32 * w + l) % g.N);  // loads: thread owns n
+          cost += warp_wavefronts(sl);
+          for (int l = 0; l < 32; ++l) sl[l] = sout((32 * w + l) % g.N);  // unpack / output: owns k
+          cost += warp_wavefronts(sl);
+        } else {
+          for (int l = 0; l < 32; ++l) {
+            const int t = 32 * w + l;
+            sl[l] = sin((t / B + 5) % g.N) + t % B;
+          }
+          cost += warp_wavefronts(sl);
+          for (int l = 0; l < 32; ++l) {
+            const int t = 32 * w + l;
+            sl[l] = sout((t / B) % g.N) + t % B;
+          }
+          cost += warp_wavefronts(sl);
+        }
+      }
+      if (best_cost < 0 || cost < best_cost) {
+        best_cost = cost;
+        bsc = sc;
+        bsr = sr;
+      }
+    }
+  }
+  g.SC = bsc;
+  g.SR = bsr;
+}
 __host__ inline size_t smem_bytes(const Geo& g) {
   return sizeof(float2) * ((size_t)g.slots() + g.tw1_len() + g.N);
 }
@@ -120,6 +206,27 @@ __device__ inline void build_tables(const Geo& g, float2* tw1, float2* tw2) {
   }
 }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): (re, im) in one 64-bit register pair.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 as_u64(float2 v) { return *reinterpret_cast<const u64*>(&v); }
+__device__ __forceinline__ float2 as_f2(u64 v) { return *reinterpret_cast<const float2*>(&v); }
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// acc += v * (w, w)
+__device__ __forceinline__ void ffma2s(u64& acc, u64 v, float w) {
+  u64 ww;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(ww) : "f"(w));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(v), "l"(ww));
+}
+
 // Stage 1 (all threads of the CTA; blockDim.x >= B*M*G).  Contains the two
 // barriers that separate reading the inputs from overwriting them in place.
 template <int M, bool INV>
@@ -129,15 +236,16 @@ __device__ inline void stage1(const Geo& g, float2* data, const float2* tw1, con
   const int b = item % g.B;
   const int n2 = (item / g.B) % M;
   const int grp = item / (g.B * M);
-  float2 A[KOUT], D[KOUT];
-  float2 x0 = make_float2(0.f, 0.f), ssum = make_float2(0.f, 0.f);
+  // packed (re, im) pairs: one FFMA2 per complex-by-real multiply-add
+  u64 A[KOUT], D[KOUT];
+  u64 x0 = 0ull, ssum = 0ull;
   if (active) {
     const float2* x = data + n2 * g.SC + b;
-    x0 = x[0];
+    x0 = as_u64(x[0]);
 #pragma unroll
     for (int t = 0; t < KOUT; ++t) {
       A[t] = x0;
-      D[t] = make_float2(0.f, 0.f);
+      D[t] = 0ull;
     }
     const float4* tw = reinterpret_cast<const float4*>(tw1 + grp * KOUT);
     const int twstride = g.G * KOUT / 2;  // float4 per j
@@ -145,24 +253,18 @@ __device__ inline void stage1(const Geo& g, float2* data, const float2* tw1, con
     const float2* xc = x + (g.P - 1) * g.SR;
 #pragma unroll 1
     for (int j = 1; j <= g.h; ++j) {
-      const float2 a = *xa, c = *xc;
+      const u64 a = as_u64(*xa), c = as_u64(*xc);
       xa += g.SR;
       xc -= g.SR;
-      const float2 s = make_float2(a.x + c.x, a.y + c.y);
-      const float2 d = make_float2(a.x - c.x, a.y - c.y);
-      ssum.x += s.x;
-      ssum.y += s.y;
+      const u64 sv = add2(a, c), dv = sub2(a, c);
+      ssum = add2(ssum, sv);
 #pragma unroll
       for (int t = 0; t < KOUT / 2; ++t) {
         const float4 w = tw[t];  // (cos, sin) of outputs 2t, 2t+1
-        A[2 * t].x = fmaf(s.x, w.x, A[2 * t].x);
-        A[2 * t].y = fmaf(s.y, w.x, A[2 * t].y);
-        D[2 * t].x = fmaf(d.x, w.y, D[2 * t].x);
-        D[2 * t].y = fmaf(d.y, w.y, D[2 * t].y);
-        A[2 * t + 1].x = fmaf(s.x, w.z, A[2 * t + 1].x);
-        A[2 * t + 1].y = fmaf(s.y, w.z, A[2 * t + 1].y);
-        D[2 * t + 1].x = fmaf(d.x, w.w, D[2 * t + 1].x);
-        D[2 * t + 1].y = fmaf(d.y, w.w, D[2 * t + 1].y);
+        ffma2s(A[2 * t], sv, w.x);
+        ffma2s(D[2 * t], dv, w.y);
+        ffma2s(A[2 * t + 1], sv, w.z);
+        ffma2s(D[2 * t + 1], dv, w.w);
       }
       tw += twstride;
     }
@@ -176,15 +278,16 @@ __device__ inline void stage1(const Geo& g, float2* data, const float2* tw1, con
       const float ws = INV ? w.y : -w.y;
       y[k1 * g.SR] = make_float2(v.x * w.x - v.y * ws, v.x * ws + v.y * w.x);
     };
-    if (grp == 0) y[0] = make_float2(x0.x + ssum.x, x0.y + ssum.y);  // k1 = 0: W = 1
+    if (grp == 0) y[0] = as_f2(add2(x0, ssum));  // k1 = 0: W = 1
 #pragma unroll
     for (int t = 0; t < KOUT; ++t) {
       const int k = grp * KOUT + 1 + t;
       if (k <= g.h) {
         // X_k = A -+ i D, X_{P-k} = A +- i D   (forward: upper signs)
-        const float2 iD = make_float2(-D[t].y, D[t].x);
-        const float2 lo = INV ? make_float2(A[t].x + iD.x, A[t].y + iD.y) : make_float2(A[t].x - iD.x, A[t].y - iD.y);
-        const float2 hi = INV ? make_float2(A[t].x - iD.x, A[t].y - iD.y) : make_float2(A[t].x + iD.x, A[t].y + iD.y);
+        const float2 At = as_f2(A[t]), Dt = as_f2(D[t]);
+        const float2 iD = make_float2(-Dt.y, Dt.x);
+        const float2 lo = INV ? make_float2(At.x + iD.x, At.y + iD.y) : make_float2(At.x - iD.x, At.y - iD.y);
+        const float2 hi = INV ? make_float2(At.x - iD.x, At.y - iD.y) : make_float2(At.x + iD.x, At.y + iD.y);
         put(k, lo);
         put(g.P - k, hi);
       }
@@ -234,9 +337,9 @@ __device__ __forceinline__ void dif_level(float2 (&v)[M]) {
 template <int M, bool INV>
 __device__ inline void stage2(const Geo& g, float2* data) {
   if (M == 1) return;
-  const int items = g.P * g.B;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int b = it % g.B, k1 = it / g.B;
+  const int kstep = blockDim.x / g.B;  // threads beyond kstep*B idle here
+  const int b = threadIdx.x % g.B;
+  for (int k1 = threadIdx.x / g.B; k1 < g.P && threadIdx.x < kstep * g.B; k1 += kstep) {
     float2* p = data + k1 * g.SR + b;
     float2 v[M];
 #pragma unroll

@@ -15,6 +15,8 @@
 //               (V,Ho,Wo,C) f32
 // Persistent CTAs loop over tiles; twiddle tables are built once per CTA.
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <cstdlib>
 #include <type_traits>
 
@@ -53,11 +55,11 @@ constexpr int U = 4;
 // carries row q (< B) in its real part and row q (>= B) in its imaginary part.
 // Threads own columns n (load) / frequencies k (unpack) so the index math is
 // done once per column; per-row offsets come from a small table.
-constexpr int MAXQ = 640;  // >= 2B for every rows plan (B <= max_threads)
+constexpr int MAXQ = 640;  // >= 2B for every rows plan (B <= rows_threads)
 constexpr int UB = 4;      // transforms per load batch (2*UB loads in flight)
 
 template <int M, int C>
-__global__ void __launch_bounds__(fft::max_threads(M)) fwd_rows_kernel(const float* __restrict__ views, int m, int H,
+__global__ void __launch_bounds__(fft::rows_threads(M), fft::rows_blocks(M)) fwd_rows_kernel(const float* __restrict__ views, int m, int H,
                                                                        int W, int pad, Geo g, int RB,
                                                                        float2* __restrict__ t1) {
   SmemPtrs s = carve(g);
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(fft::max_threads(M)) fwd_rows_kernel(const flo
 // ---------------------------------------------------------------- K0 cols
 // B is a power of two (1 << lb): b = idx & (B-1), row = idx >> lb.
 template <int M>
-__global__ void __launch_bounds__(fft::max_threads(M)) fwd_cols_kernel(const float2* __restrict__ t1, int planes,
+__global__ void __launch_bounds__(fft::cols_threads(M), fft::cols_blocks(M)) fwd_cols_kernel(const float2* __restrict__ t1, int planes,
                                                                        int H, int pad, int Whp, Geo g, int lb,
                                                                        float2* __restrict__ spec,
                                                                        double* __restrict__ partial) {
@@ -130,25 +132,24 @@ __global__ void __launch_bounds__(fft::max_threads(M)) fwd_cols_kernel(const flo
   const int N = g.N, B = g.B;
   const int cblocks = (Whp + B - 1) / B;
   const int tiles = planes * cblocks;
-  const int nload = H * B, nzero = (N - H) * B;
+  const int nzero = (N - H) * B;
   __shared__ double red[32];
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int pl = tile / cblocks, k0 = (tile % cblocks) * B;
-    const float2* src = t1 + (size_t)pl * H * Whp + k0;
+    // thread = (column b, rows y0 + t*R): pointer and slot walks, no per-element index math
+    const int b = threadIdx.x & (B - 1), R = blockDim.x >> lb, ys = threadIdx.x >> lb;
+    const bool colok = k0 + b < Whp;
+    const float2* src = t1 + ((size_t)pl * H + ys) * Whp + k0 + b;
+    const size_t step = (size_t)R * Whp;
     __syncthreads();
-    for (int base = threadIdx.x; base < nload; base += U * blockDim.x) {
+    for (int y = ys; y < H; y += U * R, src += U * step) {
       float2 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + u * blockDim.x;
-        const int b = i & (B - 1), y = i >> lb;
-        v[u] = (i < nload && k0 + b < Whp) ? __ldg(src + (size_t)y * Whp + b) : make_float2(0.f, 0.f);
-      }
+      for (int u = 0; u < U; ++u)
+        v[u] = (colok && y + u * R < H) ? __ldg(src + u * step) : make_float2(0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + u * blockDim.x;
-        if (i < nload) s.data[fft::slot_in<M>(g, (i >> lb) + pad) + (i & (B - 1))] = v[u];
-      }
+      for (int u = 0; u < U; ++u)
+        if (y + u * R < H) s.data[fft::slot_in<M>(g, y + u * R + pad) + b] = v[u];
     }
     for (int i = threadIdx.x; i < nzero; i += blockDim.x) {
       const int e = i >> lb;
@@ -159,13 +160,19 @@ __global__ void __launch_bounds__(fft::max_threads(M)) fwd_cols_kernel(const flo
     fft::stage2<M, false>(g, s.data);
     __syncthreads();
     double acc = 0.0;
-    float2* dst = spec + (size_t)pl * N * Whp + k0;
-    for (int idx = threadIdx.x; idx < N * B; idx += blockDim.x) {
-      const int b = idx & (B - 1), k = idx >> lb;
-      if (k0 + b < Whp) {
-        const float2 v = s.data[fft::slot_out(g, k) + b];
-        dst[(size_t)k * Whp + b] = v;
-        acc += (double)v.x * v.x + (double)v.y * v.y;
+    if (colok) {
+      float2* dst = spec + ((size_t)pl * N + ys) * Whp + k0 + b;
+      int k2 = g.divP.div(ys), k1 = ys - k2 * g.P;  // k = ys + t*R = k1 + P*k2
+      for (int k = ys; k < N; k += R, dst += step) {
+        const float2 v = s.data[k1 * g.SR + k2 * g.SC + b];
+        *dst = v;
+        acc = fma((double)v.x, (double)v.x, acc);
+        acc = fma((double)v.y, (double)v.y, acc);
+        k1 += R;
+        while (k1 >= g.P) {
+          k1 -= g.P;
+          ++k2;
+        }
       }
     }
     if (partial) {
@@ -193,7 +200,7 @@ __global__ void sumsq_tiles_kernel(const double* __restrict__ partial, int m, in
 
 // ---------------------------------------------------------------- K4 cols
 template <int M>
-__global__ void __launch_bounds__(fft::max_threads(M)) inv_cols_kernel(const float2* __restrict__ spec, int planes,
+__global__ void __launch_bounds__(fft::cols_threads(M), fft::cols_blocks(M)) inv_cols_kernel(const float2* __restrict__ spec, int planes,
                                                                        int Whp, int pad, int Ho, Geo g, int lb,
                                                                        float2* __restrict__ t2) {
   SmemPtrs s = carve(g);
@@ -201,40 +208,44 @@ __global__ void __launch_bounds__(fft::max_threads(M)) inv_cols_kernel(const flo
   const int N = g.N, B = g.B;
   const int cblocks = (Whp + B - 1) / B;
   const int tiles = planes * cblocks;
-  const int nload = N * B;
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int pl = tile / cblocks, k0 = (tile % cblocks) * B;
-    const float2* src = spec + (size_t)pl * N * Whp + k0;
+    const int b = threadIdx.x & (B - 1), R = blockDim.x >> lb, ys = threadIdx.x >> lb;
+    const bool colok = k0 + b < Whp;
+    const float2* src = spec + ((size_t)pl * N + ys) * Whp + k0 + b;
+    const size_t step = (size_t)R * Whp;
     __syncthreads();
-    for (int base = threadIdx.x; base < nload; base += U * blockDim.x) {
+    for (int n = ys; n < N; n += U * R, src += U * step) {
       float2 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + u * blockDim.x;
-        const int b = i & (B - 1), n = i >> lb;
-        v[u] = (i < nload && k0 + b < Whp) ? __ldg(src + (size_t)n * Whp + b) : make_float2(0.f, 0.f);
-      }
+      for (int u = 0; u < U; ++u)
+        v[u] = (colok && n + u * R < N) ? __ldg(src + u * step) : make_float2(0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + u * blockDim.x;
-        if (i < nload) s.data[fft::slot_in<M>(g, i >> lb) + (i & (B - 1))] = v[u];
-      }
+      for (int u = 0; u < U; ++u)
+        if (n + u * R < N) s.data[fft::slot_in<M>(g, n + u * R) + b] = v[u];
     }
     __syncthreads();
     fft::stage1<M, true>(g, s.data, s.tw1, s.tw2);
     fft::stage2<M, true>(g, s.data);
     __syncthreads();
-    float2* dst = t2 + (size_t)pl * Ho * Whp + k0;
-    for (int idx = threadIdx.x; idx < Ho * B; idx += blockDim.x) {
-      const int b = idx & (B - 1), y = idx >> lb;
-      if (k0 + b < Whp) dst[(size_t)y * Whp + b] = s.data[fft::slot_out(g, y + pad) + b];
+    if (colok) {
+      float2* dst = t2 + ((size_t)pl * Ho + ys) * Whp + k0 + b;
+      int k2 = g.divP.div(ys + pad), k1 = ys + pad - k2 * g.P;  // output row y = ys + t*R, index y + pad
+      for (int y = ys; y < Ho; y += R, dst += step) {
+        *dst = s.data[k1 * g.SR + k2 * g.SC + b];
+        k1 += R;
+        while (k1 >= g.P) {
+          k1 -= g.P;
+          ++k2;
+        }
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------- K4 rows
 template <int M, int C>
-__global__ void __launch_bounds__(fft::max_threads(M)) inv_rows_kernel(const float2* __restrict__ t2, int V, int Ho,
+__global__ void __launch_bounds__(fft::rows_threads(M), fft::rows_blocks(M)) inv_rows_kernel(const float2* __restrict__ t2, int V, int Ho,
                                                                        int Wo, int pad, Geo g, int RB, int srgb,
                                                                        float scale, float* __restrict__ out) {
   SmemPtrs s = carve(g);
@@ -309,19 +320,35 @@ inline size_t smem_target() {
   const char* e = getenv("FDL_FFT_SMEM_KB");
   return (e ? (size_t)atoi(e) : 100) * 1024;
 }
-inline int target_threads(int M) {
+inline int target_threads(int M, bool rows) {
+  const int cap = rows ? fft::rows_threads(M) : fft::cols_threads(M);
   const char* e = getenv("FDL_FFT_THREADS");
-  const int t = e ? atoi(e) : (M >= 32 ? 384 : 288);
-  return std::min(t, fft::max_threads(M));
+  return e ? std::min(atoi(e), cap) : cap;
 }
 
 inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// conflict-minimising strides, cached per (N, B, kind); kept only if the
+// tile still fits the shared-memory budget
+inline void tuned(Geo& g, bool rows) {
+  static thread_local std::map<std::tuple<int, int, bool>, std::pair<int, int>> cache;
+  const auto key = std::make_tuple(g.N, g.B, rows);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    Geo t = g;
+    fft::tune_strides(t, rows, ((fft::threads_for(t) + 31) / 32) * 32);
+    if (fft::smem_bytes(t) > fft::smem_bytes(g) + 4096) t = g;
+    it = cache.emplace(key, std::make_pair(t.SC, t.SR)).first;
+  }
+  g.SC = it->second.first;
+  g.SR = it->second.second;
+}
 
 // rows pass: B = RB*C/2 complex transforms, RB*C even
 bool plan_rows(int N, int C, Geo* g, int* RB) {
   int best = 0;
   const Geo g1 = fft::make_geo(N, 1);
-  const int cap = target_threads(g1.M);
+  const int cap = target_threads(g1.M, true);
   for (int rb = 1; rb <= 256; ++rb) {
     if ((rb * C) % 2) continue;
     const Geo t = fft::make_geo(N, rb * C / 2);
@@ -331,28 +358,30 @@ bool plan_rows(int N, int C, Geo* g, int* RB) {
   if (!best) {  // the smallest legal tile, if it fits at all
     const int rb = (C % 2) ? 2 : 1;
     const Geo t = fft::make_geo(N, rb * C / 2);
-    if (fft::threads_for(t) > fft::max_threads(t.M) || fft::smem_bytes(t) > 220 * 1024) return false;
+    if (fft::threads_for(t) > fft::rows_threads(t.M) || fft::smem_bytes(t) > 220 * 1024) return false;
     best = rb;
   }
   *RB = best;
   *g = fft::make_geo(N, best * C / 2);
+  tuned(*g, true);
   return true;
 }
 
 // cols pass: B a power of two (index math by shifts)
 bool plan_cols(int N, Geo* g) {
   const Geo g1 = fft::make_geo(N, 1);
-  const int cap = target_threads(g1.M);
+  const int cap = target_threads(g1.M, false);
   for (int B = 32; B >= 1; B >>= 1) {
     const Geo t = fft::make_geo(N, B);
     if (fft::threads_for(t) <= cap && fft::smem_bytes(t) <= smem_target()) {
       *g = t;
+      tuned(*g, false);
       return true;
     }
   }
   for (int B = 8; B >= 1; B >>= 1) {
     const Geo t = fft::make_geo(N, B);
-    if (fft::threads_for(t) <= fft::max_threads(t.M) && fft::smem_bytes(t) <= 220 * 1024) {
+    if (fft::threads_for(t) <= fft::cols_threads(t.M) && fft::smem_bytes(t) <= 220 * 1024) {
       *g = t;
       return true;
     }

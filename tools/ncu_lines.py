@@ -5,7 +5,8 @@ import subprocess
 import sys
 
 rep, units = sys.argv[1], float(sys.argv[2])
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kf = sys.argv[5] if len(sys.argv) > 5 else None
+out = subprocess.run(["ncu", "-i", rep] + (["-k", "regex:" + kf] if kf else []) + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
 fname = None
