@@ -127,4 +127,40 @@ __device__ inline cd cmul_rn(cd a, cd b) {
           __dadd_rn(__dmul_rn(a.re, b.im), __dmul_rn(a.im, b.re))};
 }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): (re, im) in one 64-bit register pair.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 as_u64(float2 v) { return *reinterpret_cast<const u64*>(&v); }
+__device__ __forceinline__ float2 as_f2(u64 v) { return *reinterpret_cast<const float2*>(&v); }
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// acc += v * (w, w)
+__device__ __forceinline__ void ffma2s(u64& acc, u64 v, float w) {
+  u64 ww;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(ww) : "f"(w));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(v), "l"(ww));
+}
+
+__device__ __forceinline__ u64 pack2(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void ffma2(u64& acc, u64 a, u64 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+// acc += w * z  (complex w, z): two FFMA2; the swapped / partially negated
+// operands are free operand modifiers (.LO_HI, .NP) in SASS
+__device__ __forceinline__ void cmac2(u64& acc, float wr, float wi, float2 z) {
+  ffma2(acc, pack2(z.x, z.y), pack2(wr, wr));
+  ffma2(acc, pack2(z.y, z.x), pack2(-wi, wi));
+}
+
 }  // namespace fdl

@@ -18,6 +18,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 namespace fdl {
 namespace fft {
 
@@ -204,27 +206,6 @@ __device__ inline void build_tables(const Geo& g, float2* tw1, float2* tw2) {
     sincospi(2.0 * (double)e / (double)g.N, &s, &c);
     tw2[e] = make_float2((float)c, (float)s);
   }
-}
-
-// Packed fp32 pairs (sm_100 FFMA2 / FADD2): (re, im) in one 64-bit register pair.
-typedef unsigned long long u64;
-__device__ __forceinline__ u64 as_u64(float2 v) { return *reinterpret_cast<const u64*>(&v); }
-__device__ __forceinline__ float2 as_f2(u64 v) { return *reinterpret_cast<const float2*>(&v); }
-__device__ __forceinline__ u64 add2(u64 a, u64 b) {
-  u64 r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
-  u64 r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-// acc += v * (w, w)
-__device__ __forceinline__ void ffma2s(u64& acc, u64 v, float w) {
-  u64 ww;
-  asm("mov.b64 %0, {%1, %1};" : "=l"(ww) : "f"(w));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(v), "l"(ww));
 }
 
 // Stage 1 (all threads of the CTA; blockDim.x >= B*M*G).  Contains the two

@@ -162,11 +162,11 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_t
   if (UNI) tb0 = p.tables[p.uniform_ap];
   // (made visible by the first __syncthreads of the layer loop)
 
-  float2 acc[VB][C];
+  u64 acc[VB][C];  // packed (re, im)
 #pragma unroll
   for (int b = 0; b < VB; ++b)
 #pragma unroll
-    for (int c = 0; c < C; ++c) acc[b][c] = make_float2(0.f, 0.f);
+    for (int c = 0; c < C; ++c) acc[b][c] = 0ull;
 
   float2 Lnext[C];
 #pragma unroll
@@ -219,8 +219,7 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_t
       }
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        acc[b][c].x = fmaf(wr, L[c].x, fmaf(-wi, L[c].y, acc[b][c].x));
-        acc[b][c].y = fmaf(wr, L[c].y, fmaf(wi, L[c].x, acc[b][c].y));
+        cmac2(acc[b][c], wr, wi, L[c]);
       }
     }
     __syncthreads();  // buffer k % NSTAGE is refilled by stage(k + 3)
@@ -230,7 +229,7 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_t
   for (int b = 0; b < VB; ++b) {
     if (b >= nv) break;
 #pragma unroll
-    for (int c = 0; c < C; ++c) p.out[((size_t)(v0 + b) * C + c) * Q + q] = acc[b][c];
+    for (int c = 0; c < C; ++c) p.out[((size_t)(v0 + b) * C + c) * Q + q] = as_f2(acc[b][c]);
   }
 }
 
@@ -273,11 +272,11 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_p
     cp_async_commit();
   };
 
-  float2 acc[VB][C];
+  u64 acc[VB][C];  // packed (re, im): each complex MAC is two FFMA2
 #pragma unroll
   for (int b = 0; b < VB; ++b)
 #pragma unroll
-    for (int c = 0; c < C; ++c) acc[b][c] = make_float2(0.f, 0.f);
+    for (int c = 0; c < C; ++c) acc[b][c] = 0ull;
   float2 Lnext[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) Lnext[c] = inside ? ld_stream(p.layers + (size_t)c * Q + q) : make_float2(0.f, 0.f);
@@ -307,12 +306,8 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_p
       const float w1r = fy.z * fx.z - fy.w * fx.w, w1i = fy.z * fx.w + fy.w * fx.z;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        float2& a0 = acc[2 * pr][c];
-        float2& a1 = acc[2 * pr + 1][c];
-        a0.x = fmaf(w0r, L[c].x, fmaf(-w0i, L[c].y, a0.x));
-        a0.y = fmaf(w0r, L[c].y, fmaf(w0i, L[c].x, a0.y));
-        a1.x = fmaf(w1r, L[c].x, fmaf(-w1i, L[c].y, a1.x));
-        a1.y = fmaf(w1r, L[c].y, fmaf(w1i, L[c].x, a1.y));
+        cmac2(acc[2 * pr][c], w0r, w0i, L[c]);
+        cmac2(acc[2 * pr + 1][c], w1r, w1i, L[c]);
       }
     }
   }
@@ -322,7 +317,7 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_p
   for (int b = 0; b < VB; ++b) {
     if (b >= nv) break;
 #pragma unroll
-    for (int c = 0; c < C; ++c) p.out[((size_t)(v0 + b) * C + c) * Q + q] = acc[b][c];
+    for (int c = 0; c < C; ++c) p.out[((size_t)(v0 + b) * C + c) * Q + q] = as_f2(acc[b][c]);
   }
 }
 

@@ -128,8 +128,10 @@ def test_monotone_fit_in_lambda(fdl):
 
     res = [residual(lam) for lam in (10.0, 1.0, 1e-2, 1e-4, 1e-6)]
     for a, b in zip(res, res[1:]):
-        # reference: b <= a (1 + 1e-9); fp32 renders add a ~1e-12 relative floor
-        assert b <= a * (1 + 1e-9) + 1e-11 * energy
+        # reference: b <= a (1 + 1e-9) in float64.  An fp32 render error d
+        # (|d| <= 1e-6 |image| in rms) moves sum r^2 by at most
+        # 2 |r| |d| (Cauchy-Schwarz), hence the extra term.
+        assert b <= a * (1 + 1e-9) + 2e-6 * np.sqrt(a * energy)
 
 
 def test_ridge_limit_decay(fdl):
