@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_t
   __shared__ __align__(16) AxisFactor FX[NSTAGE][VB][TX];
   __shared__ __align__(16) AxisFactor FY[NSTAGE][VB][TY];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
-  const int kx = blockIdx.x * TX + tx, ky = blockIdx.y * TY + ty;
-  const int v0 = blockIdx.z * VB;
+  const int kx = blockIdx.y * TX + tx, ky = blockIdx.z * TY + ty;
+  const int v0 = blockIdx.x * VB;
   const int nv = min(VB, p.V - v0);
   const long long Q = (long long)p.Hp * p.Whp;
   const bool inside = kx < p.Whp && ky < p.Hp;
@@ -137,13 +137,13 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_t
     for (int e = tid; e < VB * (TX + TY); e += TX * TY) {
       if (e < VB * TX) {
         const int b = e / TX, c = e % TX;
-        const int col = blockIdx.x * TX + c;
+        const int col = blockIdx.y * TX + c;
         const bool ok = b < nv && col < p.Whp;
         cp_async16(&FX[buf][b][c], p.px + (ok ? ((size_t)(v0 + b) * p.n + k) * p.Whp + col : 0), ok);
       } else {
         const int e2 = e - VB * TX;
         const int b = e2 / TY, r = e2 % TY;
-        const int row = blockIdx.y * TY + r;
+        const int row = blockIdx.z * TY + r;
         const bool ok = b < nv && row < p.Hp;
         cp_async16(&FY[buf][b][r], p.py + (ok ? ((size_t)(v0 + b) * p.n + k) * p.Hp + row : 0), ok);
       }
@@ -242,8 +242,8 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_p
   __shared__ __align__(16) float4 FX2[NSTAGE][NP][TX];
   __shared__ __align__(16) float4 FY2[NSTAGE][NP][TY];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
-  const int kx = blockIdx.x * TX + tx, ky = blockIdx.y * TY + ty;
-  const int v0 = blockIdx.z * VB;
+  const int kx = blockIdx.y * TX + tx, ky = blockIdx.z * TY + ty;
+  const int v0 = blockIdx.x * VB;
   const int npairs = min(NP, (p.V - v0 + 1) / 2);
   const long long Q = (long long)p.Hp * p.Whp;
   const bool inside = kx < p.Whp && ky < p.Hp;
@@ -256,12 +256,12 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_p
   // + NP*TY row pairs (threads < NP*TY); zero-filled outside the grid
   static_assert(NP * TX <= TX * TY, "at most one column-factor copy per thread");
   const int spr = tid / TX, sc = tid % TX;
-  const int scol = blockIdx.x * TX + sc;
+  const int scol = blockIdx.y * TX + sc;
   const bool sxact = tid < NP * TX;
   const bool sxok = sxact && spr < npairs && scol < p.Whp;
   const float4* sx = PXG + (sxok ? (size_t)(pr0 + spr) * p.n * p.Whp + scol : 0);
   const int ypr = tid / TY, yr = tid % TY;
-  const int srow = blockIdx.y * TY + yr;
+  const int srow = blockIdx.z * TY + yr;
   const bool syact = tid < NP * TY;
   const bool syok = syact && ypr < npairs && srow < p.Hp;
   const float4* sy = PYG + (syok ? (size_t)(pr0 + ypr) * p.n * p.Hp + srow : 0);
@@ -342,14 +342,16 @@ template <int C>
 int launch_sum(const RenderParams& p, cudaStream_t st) {
   constexpr int VB = C <= 3 ? 16 : 8;
   dim3 block(TX, TY);
-  dim3 grid((unsigned)((p.Whp + TX - 1) / TX), (unsigned)((p.Hp + TY - 1) / TY), (unsigned)((p.V + VB - 1) / VB));
+  // view blocks vary fastest: the CTAs that share a layer tile run together and
+  // re-read it from L2 instead of HBM (C4/C5 layers are GBs)
+  dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((p.Whp + TX - 1) / TX), (unsigned)((p.Hp + TY - 1) / TY));
   if (p.view_ap && VB == 16 && render_vb_env(true) == 8) {
-    dim3 g8(grid.x, grid.y, (unsigned)((p.V + 7) / 8));
+    dim3 g8((unsigned)((p.V + 7) / 8), grid.y, grid.z);
     launch_ap<C, 8>(p, g8, block, st);
   } else if (p.view_ap) {
     launch_ap<C, VB>(p, grid, block, st);
   } else if (VB == 16 && render_vb_env(false) == 8) {
-    dim3 g8(grid.x, grid.y, (unsigned)((p.V + 7) / 8));
+    dim3 g8((unsigned)((p.V + 7) / 8), grid.y, grid.z);
     render_pin_kernel<C, 8><<<g8, block, 0, st>>>(p);
   } else
     render_pin_kernel<C, VB><<<grid, block, 0, st>>>(p);
