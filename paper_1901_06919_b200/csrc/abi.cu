@@ -3,6 +3,7 @@
 // caches (error string, pinned staging ring, cuFFT plans).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -238,6 +239,20 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
       if (std::fabs(D->d[k] - (D->d[0] + k * delta)) > 1e-12 * dmax) uni = false;
     p.uniform_d = uni ? 1 : 0;
     p.delta = delta;
+  }
+  // one aperture for every view (mode 2 keeps its lookup constants in registers)
+  p.uniform_ap = -1;
+  if (D->view_aperture && m > 0) {
+    bool same = D->view_aperture[0] >= 0;
+    for (int j = 1; j < m && same; ++j) same = D->view_aperture[j] == D->view_aperture[0];
+    if (same) p.uniform_ap = D->view_aperture[0];
+  }
+  // K1 fast path: 4 bins per warp when the slab has enough rows to fill the
+  // GPU anyway (amortises the per-CTA tables); FDL_K1_REPS overrides
+  {
+    const long long ctas = (long long)D->nrows * ((p.Whp + 7) / 8);
+    p.reps = ctas >= 148LL * 2 * 16 ? 4 : 1;
+    if (const char* e = getenv("FDL_K1_REPS")) p.reps = std::max(1, atoi(e));
   }
 
   Blob& B = P.blob;

@@ -127,10 +127,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane >> 2, t = lane & 3;
   const int i = blockIdx.y;
-  const int kx = blockIdx.x * WARPS + warp;
   const int ky = p.rows[i];
-  const double ox = omega_x_label(kx, p.Wp), oy = omega_y_label(ky, p.Hp);
-  const bool nyq_x = (p.Wp % 2 == 0) && kx == p.Wp / 2;
+  const double oy = omega_y_label(ky, p.Hp);
   const bool nyq_y = (p.Hp % 2 == 0) && ky == p.Hp / 2;
 
   // shared layout: [PY: nv*hw complex] then per warp [PX: nu*hw complex | S 64 | T 64 | Wst NB*64 | X NP*8]
@@ -160,7 +158,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     // mode 2: the y half of every bilinear lookup depends only on (view, layer, row):
     // t_jk = scale_j (s_j - d_k), (iy, fy) of t_jk wy -- shared by the CTA's bins
     for (int e = threadIdx.x; e < p.m * p.n; e += blockDim.x) {
-      const int j = e / p.n, k = e % p.n;
+      const int j = e / p.n, k = e - j * p.n;
       const int ai = p.view_ap ? p.view_ap[j] : -1;
       YEntry ye;
       ye.ai = ai;
@@ -180,7 +178,27 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     }
   }
   __syncthreads();
-  if (kx >= p.Whp) return;  // warp-uniform; no block barriers below
+  // no block barriers below: each warp solves p.reps bins of this row,
+  // columns (blockIdx.x * reps + rep) * WARPS + warp
+  // mode 2 with one shared aperture: its lookup constants live in registers
+  const bool uap = MODE == MODE_REALA && p.uniform_ap >= 0;
+  const double2* uq = nullptr;
+  double u_xi0 = 0.0, u_inv = 0.0;
+  int u_cols = 0, u_zero = 0;
+  if (uap) {
+    const DevAperture& a0 = p.aps[p.uniform_ap];
+    uq = a0.quad;
+    u_xi0 = a0.xi0_x;
+    u_inv = a0.inv_step_x;
+    u_cols = a0.cols;
+    u_zero = a0.rows * a0.cols;
+  }
+  for (int rep = 0; rep < p.reps; ++rep) {
+  const int kx = (blockIdx.x * p.reps + rep) * WARPS + warp;
+  if (kx >= p.Whp) break;  // warp-uniform
+  const double ox = omega_x_label(kx, p.Wp);
+  const bool nyq_x = (p.Wp % 2 == 0) && kx == p.Wp / 2;
+  __syncwarp();  // the previous bin's readers of this warp's buffers are done
 
   {
     // stage this bin's m x C spectra values (one 8-byte load per view plane, all in flight)
@@ -258,7 +276,18 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
 #pragma unroll
       for (int I = 0; I < NB; ++I) {
         const int k = I * 8 + q;
-        if (valid && k < p.n) {
+        if (valid && k < p.n && uq) {
+          // shared real aperture: x half of the bilinear lookup + one quad read
+          const YEntry ye = YT[j * p.n + k];
+          const double pos = (__dmul_rn(ye.t, ox) - u_xi0) * u_inv;
+          const bool okx = (pos >= 0.0) && (pos <= (double)(u_cols - 1));
+          const int ix = okx ? min((int)pos, u_cols - 2) : 0;
+          const double fx = pos - (double)ix;
+          const int qi = okx ? min(ye.iyoff + ix, u_zero) : u_zero;
+          const double2 top = uq[2 * qi], bot = uq[2 * qi + 1];
+          const double gy = 1.0 - ye.fy, gx = 1.0 - fx;
+          mf[I] = (top.x * gy) * gx + (top.y * gy) * fx + (bot.x * ye.fy) * gx + (bot.y * ye.fy) * fx;
+        } else if (valid && k < p.n) {
           const YEntry ye = YT[j * p.n + k];
           if (ye.ai < 0) {
             mf[I] = 1.0;
@@ -544,6 +573,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     }
     p.layers[((size_t)k * p.C + c) * plane + boff] = ok ? make_float2((float)xr, (float)xi) : make_float2(nanf_, nanf_);
   }
+  }  // bins of this warp
 }
 
 template <int NB, int MODE, int ODD>
@@ -556,7 +586,8 @@ int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
   if (smem > 220 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
   auto kern = k1_fast_kernel<NB, MODE, ODD>;
   FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)((p.Whp + WARPS - 1) / WARPS), (unsigned)p.nrows);
+  if (p.reps < 1) return fail(FDL_ERR_INVALID, "K1 fast path: reps < 1");
+  dim3 grid((unsigned)((p.Whp + WARPS * p.reps - 1) / (WARPS * p.reps)), (unsigned)p.nrows);
   kern<<<grid, WARPS * 32, smem, st>>>(p, f);
   FDL_LAUNCH_CHECK("k1_fast_kernel");
   return FDL_OK;

@@ -46,6 +46,8 @@ struct SolveParams {
   float2* layers;            // (n, C, nrows, Whp)
   signed char* status;       // (nrows, Whp) or nullptr
   int uniform_d;             // d_k = d_0 + k delta (Toeplitz Gram available)
+  int uniform_ap;            // >= 0: every view uses aperture uniform_ap (mode 2 hoists its fields)
+  int reps;                  // K1 fast path: bins per warp (CTAs cover reps * 8 columns)
   double delta;
   // factored shifts: distinct u / v values (per-axis phase tables of the fast path)
   const int* fast_u_idx;
