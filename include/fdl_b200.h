@@ -124,6 +124,10 @@ typedef struct fdl_solve_desc {
   int8_t* status_dev;          /* (nrows, Whp) FDL_BIN_* or NULL */
   int32_t force_path;          /* 0 = auto; 1 = symmetric-real, 2 = real-A, 3 = complex embedding;
                                   4 = auto formulation on the generic (non-DMMA) kernel (testing) */
+  int32_t plane_rows;          /* 0: spectra/layers hold just the slab rows (buffer row i <-> rows[i]);
+                                  Hp: full-grid buffers (m or n, C, Hp, Whp) and the listed rows
+                                  are solved in place (buffer row rows[i]); status stays
+                                  (nrows, Whp).  Lets a caller solve a full spectrum in row slabs. */
 } fdl_solve_desc;
 
 /* Bytes of device workspace fdl_solve_bins needs (0 for the current kernels
@@ -175,6 +179,19 @@ int fdl_solve_dense(const fdl_dense_desc* desc, void* workspace_dev, size_t work
  * slab index of row (Hp - rows[i]) % Hp (must be in the slab). */
 int fdl_symmetrize(fdl_c64* layers_dev, int32_t n, int32_t C, int32_t Hp, int32_t Wp,
                    int32_t nrows, const int32_t* rows, const int32_t* mirror, void* stream);
+
+/* K2 on a subset of the rows of full-grid layers (n, C, Hp, Whp): every
+ * (ky, Hp-ky) pair listed in rows (host, nrows; the set must be closed under
+ * ky -> (Hp-ky) % Hp) is symmetrised as fdl_symmetrize does. */
+int fdl_symmetrize_rows(fdl_c64* layers_dev, int32_t n, int32_t C, int32_t Hp, int32_t Wp,
+                        int32_t nrows, const int32_t* rows, void* stream);
+
+/* Stream-ordered copy of the frequency rows [r0, r1) of every (layer,
+ * channel) plane of full-grid layers (planes, Hp, Whp) into the same rows of
+ * a host array of the same shape (pinned memory for asynchrony): one 2D copy.
+ * Used to overlap the read-back of finished row slabs with the solves. */
+int fdl_rows_to_host(const fdl_c64* layers_dev, fdl_c64* layers_host, int32_t planes, int32_t Hp,
+                     int32_t Whp, int32_t r0, int32_t r1, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* K3: batched render spectra   (render.py:190-207, lfmodel.py:101-122)      */

@@ -52,6 +52,7 @@ class FdlSolveDesc(ctypes.Structure):
         ("lam", ctypes.c_double), ("eps", ctypes.c_double),
         ("spectra_dev", ctypes.c_void_p), ("layers_dev", ctypes.c_void_p),
         ("status_dev", ctypes.c_void_p), ("force_path", ctypes.c_int32),
+        ("plane_rows", ctypes.c_int32),
     ]
 
 
@@ -99,6 +100,8 @@ EXPORTS = {
                                        ctypes.c_void_p]),
     "fdl_symmetrize": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 5 + [
         c_int32_p, c_int32_p, ctypes.c_void_p]),
+    "fdl_symmetrize_rows": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 5 + [c_int32_p, ctypes.c_void_p]),
+    "fdl_rows_to_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int32] * 5 + [ctypes.c_void_p]),
     "fdl_render_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlRenderDesc)]),
     "fdl_render_spectra": (ctypes.c_int, [ctypes.POINTER(FdlRenderDesc), ctypes.c_void_p,
                                           ctypes.c_size_t, ctypes.c_void_p]),

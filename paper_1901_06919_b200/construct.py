@@ -15,6 +15,7 @@ the views are sharded across GPUs.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -217,13 +218,19 @@ def aperture_table_set(apertures):
 
 
 def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps, views=None,
-               u=None, v=None, force_path=0, status=None):
-    """Run K1 on a slab of frequency rows; returns (layers (n,C,nrows,Whp) c64, n_breakdown, path)."""
+               u=None, v=None, force_path=0, status=None, out=None, full_grid=False, count=True):
+    """Run K1 on a slab of frequency rows; returns (layers (n,C,nrows,Whp) c64, n_breakdown, path).
+
+    full_grid: spectra / out are full (.., Hp, Whp) buffers and only `rows` are
+    solved, in place (plane_rows = Hp).  count=False skips the breakdown count
+    (no host synchronisation; n_breakdown is returned as None and the caller
+    inspects `status`)."""
     import torch
     device = spectra.device
     whp = Wp // 2 + 1
     nrows = len(rows)
-    layers = torch.empty((n, C, nrows, whp), dtype=torch.complex64, device=device)
+    layers = out if out is not None else torch.empty((n, C, Hp if full_grid else nrows, whp),
+                                                     dtype=torch.complex64, device=device)
     if status is None:
         status = torch.zeros((nrows, whp), dtype=torch.int8, device=device)
     rows_np = np.ascontiguousarray(rows, dtype=np.int32)
@@ -258,6 +265,7 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     desc.layers_dev = layers.data_ptr()
     desc.status_dev = status.data_ptr()
     desc.force_path = int(force_path)
+    desc.plane_rows = Hp if full_grid else 0
     L = nat.lib()
     path = L.fdl_solve_path(desc)
     if path < 0:
@@ -267,8 +275,10 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
         nat.check(L.fdl_solve_path(desc), "fdl_solve_bins_workspace")
     ws = nat.workspace(ws_bytes, device)
     nb = nat.ctypes.c_int32(0)
-    nat.check(L.fdl_solve_bins(desc, ws.data_ptr(), ws.numel(), nat.ctypes.byref(nb),
+    nat.check(L.fdl_solve_bins(desc, ws.data_ptr(), ws.numel(), nat.ctypes.byref(nb) if count else None,
                                nat.stream_handle(device)), "fdl_solve_bins")
+    if not count:
+        return layers, None, path
     n_bad = int(nb.value)
     if n_bad and lam > 0:
         # the reference's minimum-norm fallback for the flagged bins (construct.py:205-210), on the GPU
@@ -394,13 +404,16 @@ def lambda_from_sumsq(view_sumsq, Q: int, m: int) -> float:
 
 def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None, eps: float = DEFAULT_EPS,
                   pad_margin: int | None = None, chunk: int = SOLVE_CHUNK, *, device=None,
-                  force_path: int = 0) -> FdlModel:
+                  force_path: int = 0, eager_host: bool | None = None) -> FdlModel:
     """Build the disparity-layer model by per-frequency solves (construct.py:219-308).
 
     Same arguments, defaults and exceptions as the reference.  `chunk` is
     accepted and ignored (every bin is solved independently in one launch;
     results never depend on it).  `device` picks the CUDA device (default:
-    current); `force_path` pins the K1 formulation (testing).
+    current); `force_path` pins the K1 formulation (testing).  `eager_host`
+    (default: when the views came from host memory) reads the layers back to
+    pinned host memory slab by slab while later slabs solve; the model's
+    `.layers` / `layers_host()` then need no further transfer.
     """
     torch = _require_cuda()
     pu, pv, d = resolve_shifts(views, shifts)
@@ -425,14 +438,84 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
     u = views_u = None
     if shifts.is_factored:
         u, views_u = shifts.u, shifts.v
-    layers, n_bad, path = solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, lam, eps,
-                                     views=views, u=u, v=views_u, force_path=force_path)
+    if eager_host is None:
+        eager_host = not (_is_torch(views.images) and views.images.is_cuda)
+    host = None
+    if eager_host and Hp >= 4 * PIPELINE_SLABS:
+        layers, host, path = _solve_pipelined(spectra, m, n, C, Hp, Wp, pu, pv, d, lam, eps, views, u, views_u,
+                                              force_path)
+        n_bad = 0
+        if host is None:  # some bin broke down: the plain path below re-solves with the fallback
+            layers = None
+    if host is None:
+        layers, n_bad, path = solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, lam, eps,
+                                         views=views, u=u, v=views_u, force_path=force_path)
     st = last_construct_stats()
     st.path, st.breakdown_bins, st.lam = path, n_bad, float(lam)
     if n_bad:
         if lam == 0:
             raise RankDeficiencyError("singular normal matrix at some frequency")
         raise nat.FdlNativeError(f"{n_bad} bins could not be solved (minimum-norm fallback failed)")
-    symmetrize(layers, Hp, Wp)
-    return FdlModel(disparities=d, layers=layers, grid=grid, width=W, height=H, pad_margin=pad_margin,
-                    color_space=views.color_space, calibration=shifts, lambda_used=float(lam))
+    if host is None:
+        symmetrize(layers, Hp, Wp)
+    model = FdlModel(disparities=d, layers=layers, grid=grid, width=W, height=H, pad_margin=pad_margin,
+                     color_space=views.color_space, calibration=shifts, lambda_used=float(lam))
+    if host is not None:
+        model._host_async = host
+    return model
+
+
+PIPELINE_SLABS = int(os.environ.get("FDL_PIPELINE_SLABS", "4"))
+
+
+def _row_runs(rows):
+    """Maximal runs [a, b) of consecutive values of a sorted row list."""
+    runs, a = [], int(rows[0])
+    for x, y in zip(rows[:-1], rows[1:]):
+        if int(y) != int(x) + 1:
+            runs.append((a, int(x) + 1))
+            a = int(y)
+    runs.append((a, int(rows[-1]) + 1))
+    return runs
+
+
+def _solve_pipelined(spectra, m, n, C, Hp, Wp, pu, pv, d, lam, eps, views, u, v, force_path):
+    """K1 + K2 in PIPELINE_SLABS slabs of conjugate row pairs, each slab's
+    finished rows copied to pinned host memory on a side stream while the next
+    slab solves (the reference returns host layers, construct.py:300-308).
+    Returns (device layers, (host tensor, event), path), or (layers, None, path)
+    when a bin broke down (the caller re-solves with the fallback)."""
+    import torch
+    from .dist import slab_rows
+    device = spectra.device
+    whp = Wp // 2 + 1
+    layers = torch.empty((n, C, Hp, whp), dtype=torch.complex64, device=device)
+    host = torch.empty((n, C, Hp, whp), dtype=torch.complex64, pin_memory=True)
+    compute = torch.cuda.current_stream(device)
+    copy = nat.copy_stream(device)
+    L = nat.lib()
+    statuses, path = [], 0
+    for s_ in range(PIPELINE_SLABS):
+        rows, _ = slab_rows(Hp, PIPELINE_SLABS, s_)
+        if len(rows) == 0:
+            continue
+        status = torch.zeros((len(rows), whp), dtype=torch.int8, device=device)
+        statuses.append(status)
+        _, _, path = solve_slab(spectra, m, n, C, Hp, Wp, rows, pu, pv, d, lam, eps, views=views, u=u, v=v,
+                                force_path=force_path, status=status, out=layers, full_grid=True, count=False)
+        r32 = np.ascontiguousarray(rows, dtype=np.int32)
+        nat.check(L.fdl_symmetrize_rows(layers.data_ptr(), n, C, Hp, Wp, len(r32), nat.iptr(r32),
+                                        nat.stream_handle(device)), "fdl_symmetrize_rows")
+        ev = torch.cuda.Event()
+        ev.record(compute)
+        copy.wait_event(ev)
+        for a, b in _row_runs(r32):
+            nat.check(L.fdl_rows_to_host(layers.data_ptr(), host.data_ptr(), n * C, Hp, whp, a, b,
+                                         nat.ctypes.c_void_p(copy.cuda_stream)), "fdl_rows_to_host")
+    done = torch.cuda.Event()
+    done.record(copy)
+    layers.record_stream(copy)
+    if any(int(torch.count_nonzero(st_).item()) for st_ in statuses):
+        done.synchronize()
+        return layers, None, path
+    return layers, (host, done), path

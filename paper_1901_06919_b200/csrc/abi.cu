@@ -212,6 +212,9 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
   p.Wp = D->Wp;
   p.Whp = D->Wp / 2 + 1;
   p.nrows = D->nrows;
+  if (D->plane_rows != 0 && D->plane_rows != D->Hp)
+    return fail(FDL_ERR_INVALID, "plane_rows must be 0 (slab buffers) or Hp (full-grid buffers)");
+  p.plane_rows = D->plane_rows;
   p.mode = mode;
   p.h = n / 2;
   if (mode == MODE_COMPLEX) {
@@ -702,6 +705,71 @@ int fdl_solve_dense(const fdl_dense_desc* d, void* workspace_dev, size_t workspa
                             reinterpret_cast<const double2*>(d->R_dev), d->lam, reinterpret_cast<double2*>(d->x_dev),
                             d->status_dev, d->status_dev, reinterpret_cast<double*>(workspace_dev), false,
                             as_stream(stream));
+}
+
+// K2 on listed rows of full-grid layers: each pair handled from its lower ky
+__global__ void symmetrize_rows_kernel(float2* L, int planes, int Hp, int Whp, int Wp, const int* rows, int nrows) {
+  const int ncols = (Wp % 2 == 0) ? 2 : 1;
+  const long long total = (long long)planes * nrows * ncols;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(idx % ncols);
+    const long long r = idx / ncols;
+    const int ky = rows[(int)(r % nrows)];
+    const long long pl = r / nrows;
+    const int my = (Hp - ky) % Hp;
+    if (my < ky) continue;
+    const int kx = ci == 0 ? 0 : Wp / 2;
+    float2* base = L + pl * (long long)Hp * Whp;
+    const float2 a = base[(size_t)ky * Whp + kx], b = base[(size_t)my * Whp + kx];
+    const float2 na = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
+    base[(size_t)ky * Whp + kx] = na;
+    if (my != ky) base[(size_t)my * Whp + kx] = make_float2(na.x, -na.y);
+  }
+}
+
+int fdl_symmetrize_rows(fdl_c64* layers_dev, int32_t n, int32_t C, int32_t Hp, int32_t Wp, int32_t nrows,
+                        const int32_t* rows, void* stream) {
+  if (n < 1 || C < 1 || Hp < 1 || Wp < 1 || nrows < 0 || nrows > Hp || (nrows && !rows))
+    return fail(FDL_ERR_INVALID, "invalid layer shape / rows");
+  if (nrows == 0) return FDL_OK;
+  std::vector<char> in(Hp, 0);
+  for (int i = 0; i < nrows; ++i) {
+    if (rows[i] < 0 || rows[i] >= Hp) return fail(FDL_ERR_INVALID, "row out of range");
+    in[rows[i]] = 1;
+  }
+  for (int i = 0; i < nrows; ++i)
+    if (!in[(Hp - rows[i]) % Hp]) return fail(FDL_ERR_INVALID, "row set not closed under ky -> Hp - ky");
+  static thread_local int* t_rows = nullptr;
+  static thread_local size_t t_cap = 0;
+  if (t_cap < (size_t)nrows) {
+    if (t_rows) cudaFree(t_rows);
+    FDL_CUDA_CHECK(cudaMalloc(&t_rows, sizeof(int) * nrows));
+    t_cap = nrows;
+  }
+  Blob b;
+  b.add(rows, sizeof(int) * nrows);
+  cudaStream_t st = as_stream(stream);
+  int rc = upload(b, t_rows, st);
+  if (rc) return rc;
+  const long long total = (long long)n * C * nrows * ((Wp % 2 == 0) ? 2 : 1);
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  symmetrize_rows_kernel<<<std::max(blocks, 1), 256, 0, st>>>(reinterpret_cast<float2*>(layers_dev), n * C, Hp,
+                                                               Wp / 2 + 1, Wp, t_rows, nrows);
+  FDL_LAUNCH_CHECK("symmetrize_rows_kernel");
+  return FDL_OK;
+}
+
+int fdl_rows_to_host(const fdl_c64* layers_dev, fdl_c64* layers_host, int32_t planes, int32_t Hp, int32_t Whp,
+                     int32_t r0, int32_t r1, void* stream) {
+  if (!layers_dev || !layers_host || planes < 1 || Hp < 1 || Whp < 1 || r0 < 0 || r1 > Hp || r0 > r1)
+    return fail(FDL_ERR_INVALID, "invalid row window");
+  if (r0 == r1) return FDL_OK;
+  const size_t pitch = sizeof(fdl_c64) * (size_t)Hp * Whp;
+  FDL_CUDA_CHECK(cudaMemcpy2DAsync(layers_host + (size_t)r0 * Whp, pitch, layers_dev + (size_t)r0 * Whp, pitch,
+                                   sizeof(fdl_c64) * (size_t)(r1 - r0) * Whp, planes, cudaMemcpyDeviceToHost,
+                                   as_stream(stream)));
+  return FDL_OK;
 }
 
 int fdl_symmetrize(fdl_c64* layers_dev, int32_t n, int32_t C, int32_t Hp, int32_t Wp, int32_t nrows,

@@ -341,7 +341,7 @@ __global__ void build_bins_kernel(SolveParams p, const int* bins, int nb, double
   const double ox = omega_x_label(kx, p.Wp), oy = omega_y_label(ky, p.Hp);
   const bool nyq_x = (p.Wp % 2 == 0) && kx == p.Wp / 2;
   const bool nyq_y = (p.Hp % 2 == 0) && ky == p.Hp / 2;
-  const size_t plane = (size_t)p.nrows * p.Whp;
+  const size_t plane = sp_plane(p);
   for (int e = threadIdx.x; e < p.m * p.n; e += blockDim.x) {
     const int j = e / p.n, k = e % p.n;
     const cd a = system_entry(p, j, k, kx, ky, ox, oy, nyq_x, nyq_y);
@@ -349,7 +349,7 @@ __global__ void build_bins_kernel(SolveParams p, const int* bins, int nb, double
   }
   for (int e = threadIdx.x; e < p.m * p.C; e += blockDim.x) {
     const int j = e / p.C, c = e % p.C;
-    const float2 v = p.spectra[((size_t)j * p.C + c) * plane + (size_t)i * p.Whp + kx];
+    const float2 v = p.spectra[((size_t)j * p.C + c) * plane + sp_boff(p, i, kx)];
     b[(size_t)t * p.m * p.C + e] = make_double2(v.x, v.y);
   }
   const double osq = ox * ox + oy * oy;
@@ -362,11 +362,11 @@ __global__ void scatter_bins_kernel(SolveParams p, const int* bins, int nb, cons
   if (t >= nb) return;
   const long long bin = bins[t];
   const int i = (int)(bin / p.Whp), kx = (int)(bin % p.Whp);
-  const size_t plane = (size_t)p.nrows * p.Whp;
+  const size_t plane = sp_plane(p);
   for (int e = threadIdx.x; e < p.n * p.C; e += blockDim.x) {
     const int k = e / p.C, c = e % p.C;
     const double2 v = x[(size_t)t * p.n * p.C + e];
-    p.layers[((size_t)k * p.C + c) * plane + (size_t)i * p.Whp + kx] = make_float2((float)v.x, (float)v.y);
+    p.layers[((size_t)k * p.C + c) * plane + sp_boff(p, i, kx)] = make_float2((float)v.x, (float)v.y);
   }
   if (threadIdx.x == 0 && p.status) p.status[bin] = st[t] == 2 ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
 }

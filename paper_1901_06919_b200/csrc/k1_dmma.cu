@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
 
   {
     // stage this bin's m x C spectra values (one 8-byte load per view plane, all in flight)
-    const size_t plane_ = (size_t)p.nrows * p.Whp;
-    const float2* src = p.spectra + (size_t)i * p.Whp + kx;
+    const size_t plane_ = sp_plane(p);
+    const float2* src = p.spectra + sp_boff(p, i, kx);
     for (int e = lane; e < p.m * p.C; e += 32) BS[e] = src[(size_t)e * plane_];
   }
   if (MODE == MODE_SYMREAL) {
@@ -219,8 +219,9 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
 #pragma unroll
   for (int b = 0; b < NB; ++b) r[b][0] = r[b][1] = 0.0;
 
-  const size_t plane = (size_t)p.nrows * p.Whp;
-  const size_t boff = (size_t)i * p.Whp + kx;
+  const size_t plane = sp_plane(p);
+  const size_t boff = sp_boff(p, i, kx);      // spectra / layers
+  const size_t soff = (size_t)i * p.Whp + kx;  // status (slab-indexed)
   const int h = p.h;
   // Toeplitz-Hankel Gram (mode 1, uniform d, off the Nyquist lines, <= 3 channels):
   // G' follows from t[r] = sum_j conj(A_j0) A_jr, which the RHS DMMAs produce for
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     if ((idx & 7) < 2 * p.C) finite = finite && isfinite(X[idx]);
   }
   ok = __all_sync(FULL, finite) && ok;
-  if (p.status && lane == 0) p.status[boff] = ok ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
+  if (p.status && lane == 0) p.status[soff] = ok ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
   const float nanf_ = __int_as_float(0x7fc00000);
   for (int e = lane; e < p.n * p.C; e += 32) {
     const int k = e / p.C, c = e % p.C;

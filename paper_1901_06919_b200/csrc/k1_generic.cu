@@ -14,8 +14,8 @@ __device__ void build_row(const SolveParams& p, int r, int i, int kx, int ky, do
   const double oy = omega_y_label(ky, p.Hp);
   const bool nyq_x = (p.Wp % 2 == 0) && kx == p.Wp / 2;
   const bool nyq_y = (p.Hp % 2 == 0) && ky == p.Hp / 2;
-  const size_t plane = (size_t)p.nrows * p.Whp;
-  const size_t boff = (size_t)i * p.Whp + kx;
+  const size_t plane = sp_plane(p);
+  const size_t boff = sp_boff(p, i, kx);
   if (p.mode == MODE_SYMREAL) {
     const int j = r;
     for (int q = 0; q < p.h; ++q) {
@@ -133,8 +133,8 @@ __global__ void k1_generic_kernel(SolveParams p) {
     __syncwarp();
   }
 
-  const size_t plane = (size_t)p.nrows * p.Whp;
-  const size_t boff = (size_t)i * p.Whp + kx;
+  const size_t plane = sp_plane(p);
+  const size_t boff = sp_boff(p, i, kx);
   if (!ok) {
     if (p.status && lane == 0) p.status[bin] = FDL_BIN_BREAKDOWN;
     const float nanf_ = __int_as_float(0x7fc00000);

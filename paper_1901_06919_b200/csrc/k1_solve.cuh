@@ -48,6 +48,7 @@ struct SolveParams {
   int uniform_d;             // d_k = d_0 + k delta (Toeplitz Gram available)
   int uniform_ap;            // >= 0: every view uses aperture uniform_ap (mode 2 hoists its fields)
   int reps;                  // K1 fast path: bins per warp (CTAs cover reps * 8 columns)
+  int plane_rows;            // 0: slab buffers (row i); > 0: full-grid buffers of plane_rows rows (row rows[i])
   double delta;
   // factored shifts: distinct u / v values (per-axis phase tables of the fast path)
   const int* fast_u_idx;
@@ -57,6 +58,14 @@ struct SolveParams {
   int fast_nu, fast_nv;
   double* fast_tables;       // workspace for the per-axis phase tables (fast path)
 };
+
+// spectra / layers addressing: slab buffers or full-grid buffers (plane_rows)
+__device__ __forceinline__ size_t sp_plane(const SolveParams& p) {
+  return (size_t)(p.plane_rows ? p.plane_rows : p.nrows) * p.Whp;
+}
+__device__ __forceinline__ size_t sp_boff(const SolveParams& p, int i, int kx) {
+  return (size_t)(p.plane_rows ? p.rows[i] : i) * p.Whp + kx;
+}
 
 // A_jk (construct.py:168-180 with build_system_row's Nyquist handling, construct.py:83-109)
 __device__ inline cd system_entry(const SolveParams& p, int j, int k, int kx, int ky, double ox, double oy,

@@ -88,3 +88,25 @@ def test_construct_sharded_world1_matches_construct_fdl(cuda):
         assert torch.equal(full, ref.layers_device())
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_pipelined_readback_bitwise():
+    """construct_fdl from host views solves in conjugate-row slabs with the
+    read-back overlapped (plane_rows = Hp, fdl_symmetrize_rows,
+    fdl_rows_to_host); layers must be bit-identical to the one-launch path and
+    the host copy to the device layers."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1901_06919_b200 as fdl
+    from harness.synth import make_case
+    case = make_case("c2", size=96)
+    views = fdl.ViewSet(images=case.views.numpy(), u=case.u, v=case.v)
+    sh = fdl.ShiftParams.factored(case.u, case.v, case.d)
+    a = fdl.construct_fdl(views, sh, eager_host=True)
+    b = fdl.construct_fdl(views, sh, eager_host=False)
+    assert a._host_async is not None and b._host_async is None
+    assert torch.equal(a.layers_device(), b.layers_device())
+    assert torch.equal(a.layers_host(), b.layers_device().cpu())
+    np.testing.assert_array_equal(a.layers, b.layers)
