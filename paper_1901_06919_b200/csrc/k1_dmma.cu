@@ -29,6 +29,10 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int WARPS = 8;  // bins (consecutive kx of one row) per CTA
+// Row stride (doubles) of the per-warp 8x8 scratch blocks (S, T, W) and of X:
+// 12 makes the DMMA-fragment-layout reads/writes ([q][t], [t][q], [q][2t])
+// conflict-free (8 would put rows q and q+2 on the same banks).
+constexpr int LD = 8;
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -69,8 +73,8 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
 
 __device__ __forceinline__ void store_c(double* S, const double (&c)[2], int lane) {
   const int q = lane >> 2, t = lane & 3;
-  S[q * 8 + 2 * t] = c[0];
-  S[q * 8 + 2 * t + 1] = c[1];
+  S[q * LD + 2 * t] = c[0];
+  S[q * LD + 2 * t + 1] = c[1];
 }
 
 struct FastParams {
@@ -81,6 +85,8 @@ struct FastParams {
   int nu, nv;
   int H8;               // columns per cos/sin half, multiple of 8 (mode 1)
   int hw;               // phase-table width: h + (n odd)
+  int hwp;              // shared-memory row pitch of the tables (double2): = 2 mod 8, so the
+                        // 4 views x 2 layers of a quarter-warp hit distinct banks
   const double2* px_all;  // (Whp, nu, hw) exp(2 pi i fl(u d_p) wx), cosine on the Nyquist column
   const double2* py_all;  // (nrows, nv, hw)
 };
@@ -133,27 +139,30 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
 
   // shared layout: [PY: nv*hw complex] then per warp [PX: nu*hw complex | S 64 | T 64 | Wst NB*64 | X NP*8]
   double* PY = smem;
-  const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hw : 0;
-  const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hw : 0;
+  const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
+  const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
   const int m4 = (p.m + 3) & ~3;
   const int ro_words = (MODE == MODE_SYMREAL) ? m4 : 3 * p.m * p.n;  // mode 2: YEntry per (view, layer)
   int2* ROWOFF = reinterpret_cast<int2*>(PY + py_words);
   YEntry* YT = reinterpret_cast<YEntry*>(PY + py_words);
   const int bs_words = (p.m * p.C + 1) & ~1;  // staged spectra, one float2 per (view, channel); keeps 16-B alignment
-  const int per_warp = px_words + 64 + 64 + NB * 64 + NP * 8 + bs_words;
+  const int per_warp = px_words + 8 * LD + 8 * LD + NB * 8 * LD + NP * LD + bs_words;
   double* base = smem + py_words + ro_words + warp * per_warp;
   double* PX = base;
   double* S = PX + px_words;
-  double* T = S + 64;
-  double* Wst = T + 64;
-  double* X = Wst + NB * 64;
-  float2* BS = reinterpret_cast<float2*>(X + NP * 8);
+  double* T = S + 8 * LD;
+  double* Wst = T + 8 * LD;
+  double* X = Wst + NB * 8 * LD;
+  float2* BS = reinterpret_cast<float2*>(X + NP * LD);
 
   if (MODE == MODE_SYMREAL) {
     const double2* src = f.py_all + (size_t)i * f.nv * f.hw;
-    for (int e = threadIdx.x; e < f.nv * f.hw; e += blockDim.x) reinterpret_cast<double2*>(PY)[e] = src[e];
+    for (int e = threadIdx.x; e < f.nv * f.hw; e += blockDim.x) {
+      const int rr = e / f.hw;
+      reinterpret_cast<double2*>(PY)[rr * f.hwp + (e - rr * f.hw)] = src[e];
+    }
     for (int e = threadIdx.x; e < m4; e += blockDim.x)
-      ROWOFF[e] = e < p.m ? make_int2(f.u_idx[e] * f.hw, f.v_idx[e] * f.hw) : make_int2(0, 0);
+      ROWOFF[e] = e < p.m ? make_int2(f.u_idx[e] * f.hwp, f.v_idx[e] * f.hwp) : make_int2(0, 0);
   } else {
     // mode 2: the y half of every bilinear lookup depends only on (view, layer, row):
     // t_jk = scale_j (s_j - d_k), (iy, fy) of t_jk wy -- shared by the CTA's bins
@@ -208,7 +217,10 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
   }
   if (MODE == MODE_SYMREAL) {
     const double2* src = f.px_all + (size_t)kx * f.nu * f.hw;
-    for (int e = lane; e < f.nu * f.hw; e += 32) reinterpret_cast<double2*>(PX)[e] = src[e];
+    for (int e = lane; e < f.nu * f.hw; e += 32) {
+      const int rr = e / f.hw;
+      reinterpret_cast<double2*>(PX)[rr * f.hwp + (e - rr * f.hw)] = src[e];
+    }
   }
   __syncwarp();
 
@@ -331,8 +343,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     // RHS columns 6/7 = M^T [Re A_0, Im A_0]  ->  t[r], r = 0..n-1  ->  G fragments
 #pragma unroll
     for (int I = 0; I < NB; ++I) {
-      X[(I * 8 + q) * 8 + 2 * t] = r[I][0];
-      X[(I * 8 + q) * 8 + 2 * t + 1] = r[I][1];
+      X[(I * 8 + q) * LD + 2 * t] = r[I][0];
+      X[(I * 8 + q) * LD + 2 * t + 1] = r[I][1];
     }
     __syncwarp();
     double* TT = S;  // S and T are contiguous: 2 * 64 doubles = t[0..63]
@@ -340,15 +352,15 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     for (int rr = lane; rr < p.n; rr += 32) {
       double re, im;
       if (ODD && rr == h) {
-        re = X[(2 * H8) * 8 + 6];
-        im = -X[(2 * H8) * 8 + 7];
+        re = X[(2 * H8) * LD + 6];
+        im = -X[(2 * H8) * LD + 7];
       } else if (rr < h) {
-        re = X[rr * 8 + 6] - X[(H8 + rr) * 8 + 7];
-        im = -X[(H8 + rr) * 8 + 6] - X[rr * 8 + 7];
+        re = X[rr * LD + 6] - X[(H8 + rr) * LD + 7];
+        im = -X[(H8 + rr) * LD + 6] - X[rr * LD + 7];
       } else {
         const int pq = p.n - 1 - rr;
-        re = X[pq * 8 + 6] + X[(H8 + pq) * 8 + 7];
-        im = X[(H8 + pq) * 8 + 6] - X[pq * 8 + 7];
+        re = X[pq * LD + 6] + X[(H8 + pq) * LD + 7];
+        im = X[(H8 + pq) * LD + 6] - X[pq * LD + 7];
       }
       TT[2 * rr] = re;
       TT[2 * rr + 1] = im;
@@ -435,7 +447,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     if (lane < 8) {
       double a[8], dinv[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) a[c] = S[lane * 8 + c];
+      for (int c = 0; c < 8; ++c) a[c] = S[lane * LD + c];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const double akk = __shfl_sync(0xffu, a[k], k);
@@ -448,7 +460,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
         for (int c = k + 1; c < 8; ++c) a[c] = fma(-a[k], __shfl_sync(0xffu, a[k], c), a[c]);  // upper: harmless
       }
 #pragma unroll
-      for (int c = 0; c < 8; ++c) S[lane * 8 + c] = a[c];  // upper triangle ignored below
+      for (int c = 0; c < 8; ++c) S[lane * LD + c] = a[c];  // upper triangle ignored below
       __syncwarp(0xffu);
       // column `lane` of W = L^-1: w_rr = (delta_rc - sum_{k<rr} L_rk w_k) / L_rr  (zero above c)
       const int c = lane;
@@ -457,17 +469,17 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
       for (int rr = 0; rr < 8; ++rr) {
         double acc = (rr == c) ? 1.0 : 0.0;
 #pragma unroll
-        for (int k = 0; k < rr; ++k) acc = fma(-S[rr * 8 + k], w[k], acc);
+        for (int k = 0; k < rr; ++k) acc = fma(-S[rr * LD + k], w[k], acc);
         w[rr] = acc * dinv[rr];
       }
 #pragma unroll
-      for (int rr = 0; rr < 8; ++rr) Wst[K * 64 + rr * 8 + c] = w[rr];
+      for (int rr = 0; rr < 8; ++rr) Wst[K * 8 * LD + rr * LD + c] = w[rr];
     }
     ok = ok && __all_sync(FULL, lok);
     __syncwarp();
-    const double* Wk = Wst + K * 64;
+    const double* Wk = Wst + K * 8 * LD;
     // A-fragment of W (= B-fragment of W^T): W[q][t], W[q][4+t]
-    const double wa0 = Wk[q * 8 + t], wa1 = Wk[q * 8 + 4 + t];
+    const double wa0 = Wk[q * LD + t], wa1 = Wk[q * LD + 4 + t];
 
     // (b) panel L_IK = G_IK W^T, kept in place (accumulator layout) and as A-fragments
     double lf[NB][2];
@@ -494,7 +506,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     store_c(T, r[K], lane);
     __syncwarp();
     {
-      const double b0 = T[t * 8 + q], b1 = T[(4 + t) * 8 + q];
+      const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
       double y[2] = {0.0, 0.0};
       dmma(y, wa0, b0);
       dmma(y, wa1, b1);
@@ -505,7 +517,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     store_c(T, r[K], lane);
     __syncwarp();
     {
-      const double b0 = T[t * 8 + q], b1 = T[(4 + t) * 8 + q];
+      const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
 #pragma unroll
       for (int I = K + 1; I < NB; ++I) {
         dmma(r[I], -lf[I][0], b0);
@@ -523,21 +535,21 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     for (int I = K + 1; I < NB; ++I) {
       double a0, a1;
       c_to_at(g[blk(I, K)], a0, a1, lane);  // L_IK^T
-      const double b0 = X[(I * 8 + t) * 8 + q], b1 = X[(I * 8 + 4 + t) * 8 + q];
+      const double b0 = X[(I * 8 + t) * LD + q], b1 = X[(I * 8 + 4 + t) * LD + q];
       dmma(z, -a0, b0);
       dmma(z, -a1, b1);
     }
     store_c(T, z, lane);
     __syncwarp();
-    const double* Wk = Wst + K * 64;
-    const double at0 = Wk[t * 8 + q], at1 = Wk[(4 + t) * 8 + q];  // W^T A-fragment
-    const double b0 = T[t * 8 + q], b1 = T[(4 + t) * 8 + q];
+    const double* Wk = Wst + K * 8 * LD;
+    const double at0 = Wk[t * LD + q], at1 = Wk[(4 + t) * LD + q];  // W^T A-fragment
+    const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
     double x[2] = {0.0, 0.0};
     dmma(x, at0, b0);
     dmma(x, at1, b1);
     __syncwarp();
-    X[(K * 8 + q) * 8 + 2 * t] = x[0];
-    X[(K * 8 + q) * 8 + 2 * t + 1] = x[1];
+    X[(K * 8 + q) * LD + 2 * t] = x[0];
+    X[(K * 8 + q) * LD + 2 * t + 1] = x[1];
     __syncwarp();
   }
 
@@ -546,7 +558,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
 #pragma unroll
   for (int e = 0; e < NP * 8 / 32; ++e) {
     const int idx = e * 32 + lane;
-    if ((idx & 7) < 2 * p.C) finite = finite && isfinite(X[idx]);
+    if ((idx & 7) < 2 * p.C) finite = finite && isfinite(X[(idx >> 3) * LD + (idx & 7)]);
   }
   ok = __all_sync(FULL, finite) && ok;
   if (p.status && lane == 0) p.status[soff] = ok ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
@@ -557,20 +569,20 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     if (MODE == MODE_SYMREAL) {
       const int H8 = NBc * 8;
       if (ODD && k == h) {
-        xr = X[(2 * H8) * 8 + 2 * c];
-        xi = X[(2 * H8) * 8 + 2 * c + 1];
+        xr = X[(2 * H8) * LD + 2 * c];
+        xi = X[(2 * H8) * LD + 2 * c + 1];
       } else {
         const bool hi = k >= h;
         const int pp = hi ? p.n - 1 - k : k;
         // v+ = aa + i bb, v- = cc + i dd;  x_p = (v+ + i v-)/2, x_{n-1-p} = (v+ - i v-)/2
-        const double aa = X[pp * 8 + 2 * c], bb = X[pp * 8 + 2 * c + 1];
-        const double cc = X[(H8 + pp) * 8 + 2 * c], dd = X[(H8 + pp) * 8 + 2 * c + 1];
+        const double aa = X[pp * LD + 2 * c], bb = X[pp * LD + 2 * c + 1];
+        const double cc = X[(H8 + pp) * LD + 2 * c], dd = X[(H8 + pp) * LD + 2 * c + 1];
         xr = 0.5 * (hi ? aa + dd : aa - dd);
         xi = 0.5 * (hi ? bb - cc : bb + cc);
       }
     } else {
-      xr = X[k * 8 + 2 * c];
-      xi = X[k * 8 + 2 * c + 1];
+      xr = X[k * LD + 2 * c];
+      xi = X[k * LD + 2 * c + 1];
     }
     p.layers[((size_t)k * p.C + c) * plane + boff] = ok ? make_float2((float)xr, (float)xi) : make_float2(nanf_, nanf_);
   }
@@ -579,11 +591,11 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
 
 template <int NB, int MODE, int ODD>
 int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
-  const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hw : 0;
-  const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hw : 0;
+  const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
+  const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
   const int ro_words = (MODE == MODE_SYMREAL) ? ((p.m + 3) & ~3) : 3 * p.m * p.n;
   const size_t smem = sizeof(double) * ((size_t)py_words + ro_words +
-                                        (size_t)WARPS * (px_words + 128 + NB * 64 + NB * 64 + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
+                                        (size_t)WARPS * (px_words + 16 * LD + NB * 8 * LD + NB * 8 * LD + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
   if (smem > 220 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
   auto kern = k1_fast_kernel<NB, MODE, ODD>;
   FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -673,6 +685,7 @@ int k1_fast_launch(const SolveParams& p, cudaStream_t st, bool* handled) {
     NB = 2 * f.H8 / 8 + (p.n & 1);
     f.hw = h + (p.n & 1);
     if (f.hw == 0) return FDL_OK;
+    f.hwp = f.hw + ((2 - f.hw % 8) + 8) % 8;
     // distinct u / v values (uploaded with the parameter block by the caller)
     if (!p.fast_u_idx || !p.fast_tables) return FDL_OK;
     f.u_idx = p.fast_u_idx;
