@@ -37,6 +37,7 @@ def build(force: bool = False, verbose: bool = True) -> Path:
         obj = OUT.parent / (src.stem + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xptxas", "-O3", "-I", str(ROOT / "include"), "-I", str(CSRC),
+               *os.environ.get("FDL_NVCC_EXTRA", "").split(),  # A/B experiments (-D...)
                "-c", str(src), "-o", str(obj)]
         jobs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(str(obj))

@@ -33,6 +33,10 @@ constexpr int WARPS = 8;  // bins (consecutive kx of one row) per CTA
 // 12 makes the DMMA-fragment-layout reads/writes ([q][t], [t][q], [q][2t])
 // conflict-free (8 would put rows q and q+2 on the same banks).
 constexpr int LD = 8;
+#ifndef FDL_K1_KUNROLL
+#define FDL_K1_KUNROLL 2
+#endif
+constexpr int kKUnroll = FDL_K1_KUNROLL;  // k-step loop unroll (A/B builds)
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -336,6 +340,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     }
   };
   const int mfull = p.m & ~3;
+#pragma unroll kKUnroll
   for (int r0 = 0; r0 < mfull; r0 += 4) kstep(r0, false);
   if (mfull < p.m) kstep(mfull, true);
 
