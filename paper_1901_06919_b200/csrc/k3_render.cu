@@ -9,6 +9,7 @@
 // (view, bin, layer), one complex product of the two axis phases, an optional
 // 2x2 bilinear gather from the float32 table and the complex MAC over
 // channels, all in float32 (>= 83 dB).
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -39,13 +40,16 @@ __global__ void render_factors_kernel(RenderParams p) {
     f.re = (float)ph.re;
     f.im = (float)ph.im;
     f.frac = 0.f;
-    f.idx = 0;
+    f.idx = p.fast_ap ? p.dq_one : 0;
     if (ai >= 0) {
       const DevAperture& ap = p.aps[ai];
       int i0;
       double fr;
       bool ok = axis_lookup(t * ox, ap.xi0_x, ap.step_x, ap.cols, i0, fr);
-      f.idx = ok ? i0 : ap.rows * ap.cols;  // quad-table column; out of range -> the zero entry
+      if (p.fast_ap)
+        f.idx = ok ? p.ap_qbase[ai] + i0 : p.dq_zero;
+      else
+        f.idx = ok ? i0 : ap.rows * ap.cols;  // quad-table column; out of range -> the zero entry
       f.frac = (float)fr;
       bad_x += ok ? 0 : 1;
     }
@@ -67,7 +71,10 @@ __global__ void render_factors_kernel(RenderParams p) {
       int i0;
       double fr;
       bool ok = axis_lookup(t * oy, ap.xi0_y, ap.step_y, ap.rows, i0, fr);
-      f.idx = ok ? i0 * ap.cols : ap.rows * ap.cols;  // quad-table row offset
+      if (p.fast_ap)
+        f.idx = ok ? i0 * ap.cols : p.dq_zero;
+      else
+        f.idx = ok ? i0 * ap.cols : ap.rows * ap.cols;  // quad-table row offset
       f.frac = (float)fr;
       bad_y += ok ? 0 : 1;
     }
@@ -321,6 +328,491 @@ __global__ void __launch_bounds__(TX * TY, (VB <= 8 && C <= 3) ? 3 : 2) render_p
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fast tiles.  CTA = 256 threads over 32 columns x 8 rows of bins; each warp
+// covers 8 columns x 4 rows, so a warp's per-(view, layer) column factors are 8
+// distinct 16-byte words and its row factors 4 (one shared-memory wavefront
+// each, the rest broadcast).  All per-(view, bin, layer) arithmetic is packed
+// fp32 (FFMA2/FMUL2 with a broadcast scalar operand):
+//   pinhole:  w = py * px                          FMUL2 + FFMA2
+//   aperture: (A, B) = (a, b) + fy (c, d)          FFMA2
+//             s = A + fx B                         FFMA
+//             w = s * (py * px)                    FMUL2 + FFMA2 + FMUL2
+//   each channel: acc += w * L                     2 FFMA2
+// ---------------------------------------------------------------------------
+constexpr int FX_T = 32, FY_T = 8;
+
+__device__ __forceinline__ u64 fmul2s(u64 a, float s) {
+  u64 r, ss;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(ss) : "f"(s));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(ss));
+  return r;
+}
+// acc + (-a.y, a.x) * s   (i * a * s)
+__device__ __forceinline__ u64 ffma2_i(u64 acc, u64 a, float s) {
+  const float2 f = as_f2(a);
+  u64 r = acc;
+  ffma2s(r, pack2(-f.y, f.x), s);
+  return r;
+}
+// complex product of two (re, im) pairs, packed: x * y
+__device__ __forceinline__ u64 cmul2(float2 x, float2 y) {
+  return ffma2_i(fmul2s(pack2(x.x, x.y), y.x), pack2(x.x, x.y), y.y);
+}
+// acc += w * L  (two FFMA2, L components broadcast)
+__device__ __forceinline__ void cmac_w(u64& acc, u64 w, float2 L) {
+  ffma2s(acc, w, L.x);
+  acc = ffma2_i(acc, w, L.y);
+}
+
+__device__ __forceinline__ int fast_col(int tid) { return ((tid >> 5) & 3) * 8 + (tid & 7); }
+__device__ __forceinline__ int fast_row(int tid) { return (tid >> 7) * 4 + ((tid >> 3) & 3); }
+
+// 8-byte asynchronous copy (layer values: rows of an odd-width half spectrum
+// are not 16-byte aligned); zero-filled when !valid
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int src_size = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(gsrc), "r"(src_size));
+}
+
+// pinhole batch: view-pair interleaved phases (same factor layout as render_pin_kernel).
+// Per-layer staging: every thread copies its own bin's C layer values and
+// XPT column-factor / at most one row-factor 16-byte word into ring slot
+// k % NSTAGE; source pointers are formed once, a layer step adds a stride.
+template <int C, int VB>
+__global__ void __launch_bounds__(256, 2) render_pin_fast(RenderParams p) {
+  constexpr int NP = VB / 2;
+  static_assert(NP * FY_T <= 256, "one row-factor copy per thread");
+  constexpr int XPT = (NP * FX_T + 255) / 256;
+  struct __align__(16) Slot {
+    float4 fx[NP][FX_T];
+    float4 fy[NP][FY_T];
+    float2 L[C][256];
+  };
+  __shared__ Slot S[NSTAGE];
+  const int tid = threadIdx.x;
+  const int lx = fast_col(tid), ly = fast_row(tid);
+  const int kx = blockIdx.y * FX_T + lx, ky = blockIdx.z * FY_T + ly;
+  const int v0 = blockIdx.x * VB;
+  const int npairs = min(NP, (p.V - v0 + 1) / 2);
+  const long long Q = (long long)p.Hp * p.Whp;
+  const bool inside = kx < p.Whp && ky < p.Hp;
+  const long long q = inside ? (long long)ky * p.Whp + kx : 0;
+  const float4* PXG = reinterpret_cast<const float4*>(p.px);
+  const float4* PYG = reinterpret_cast<const float4*>(p.py);
+
+  const char* xsrc[XPT];
+  int xdst[XPT];
+  bool xok[XPT], xact[XPT];
+#pragma unroll
+  for (int i = 0; i < XPT; ++i) {
+    const int e = tid + 256 * i;
+    const int pr = e / FX_T, c = e % FX_T, col = blockIdx.y * FX_T + c;
+    xact[i] = e < NP * FX_T;
+    xok[i] = xact[i] && pr < npairs && col < p.Whp;
+    xsrc[i] = reinterpret_cast<const char*>(PXG + (xok[i] ? (size_t)(v0 / 2 + pr) * p.n * p.Whp + col : 0));
+    xdst[i] = (int)((char*)&S[0].fx[pr % NP][c] - (char*)&S[0]);
+  }
+  const long long xstep = (long long)p.Whp * 16;
+  const int ypr = tid / FY_T, yr = tid % FY_T, row = blockIdx.z * FY_T + yr;
+  const bool yact = tid < NP * FY_T;
+  const bool yok = yact && ypr < npairs && row < p.Hp;
+  const char* ysrc = reinterpret_cast<const char*>(PYG + (yok ? (size_t)(v0 / 2 + ypr) * p.n * p.Hp + row : 0));
+  const long long ystep = (long long)p.Hp * 16;
+  const int ydst = (int)((char*)&S[0].fy[ypr % NP][yr] - (char*)&S[0]);
+  const float2* lsrc0 = p.layers + q;
+  const long long lstep = inside ? (long long)C * Q : 0;
+  auto stage = [&](int k) {
+    char* base = reinterpret_cast<char*>(&S[k % NSTAGE]);
+#pragma unroll
+    for (int i = 0; i < XPT; ++i)
+      if (xact[i]) cp_async16(base + xdst[i], xsrc[i] + (xok[i] ? k * xstep : 0), xok[i]);
+    if (yact) cp_async16(base + ydst, ysrc + (yok ? k * ystep : 0), yok);
+    const float2* ls = lsrc0 + k * lstep;
+#pragma unroll
+    for (int c = 0; c < C; ++c) cp_async8(&S[k % NSTAGE].L[c][tid], ls + c * Q, inside);
+    cp_async_commit();
+  };
+
+  u64 acc[VB][C];
+#pragma unroll
+  for (int b = 0; b < VB; ++b)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[b][c] = 0ull;
+  stage(0);
+  if (p.n > 1) stage(1);
+  for (int k = 0; k < p.n; ++k) {
+    const Slot& sl = S[k % NSTAGE];
+    if (k + 1 < p.n) cp_async_wait<1>(); else cp_async_wait<0>();
+    __syncthreads();  // layer k visible; everyone is done with layer k-1's slot
+    if (k + 2 < p.n) stage(k + 2);
+    float2 L[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) L[c] = sl.L[c][tid];
+    float4 x = sl.fx[0][lx], y = sl.fy[0][ly];
+#pragma unroll
+    for (int pr = 0; pr < NP; ++pr) {
+      float4 xn, yn;
+      if (pr + 1 < NP) {
+        xn = sl.fx[pr + 1][lx];
+        yn = sl.fy[pr + 1][ly];
+      }
+      const u64 w0 = cmul2(make_float2(x.x, x.y), make_float2(y.x, y.y));
+      const u64 w1 = cmul2(make_float2(x.z, x.w), make_float2(y.z, y.w));
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        cmac_w(acc[2 * pr][c], w0, L[c]);
+        cmac_w(acc[2 * pr + 1][c], w1, L[c]);
+      }
+      if (pr + 1 < NP) {
+        x = xn;
+        y = yn;
+      }
+    }
+  }
+  if (!inside) return;
+  const int nv = min(VB, p.V - v0);
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    if (b >= nv) break;
+#pragma unroll
+    for (int c = 0; c < C; ++c) p.out[((size_t)(v0 + b) * C + c) * Q + q] = as_f2(acc[b][c]);
+  }
+}
+
+// real-table batch (any mix of real apertures and pinhole views): per-view
+// factors {re, im, frac, absolute idx}; the 2x2 quad of (view b, layer k+1)
+// is gathered into registers while layer k is consumed.
+template <int C, int VB>
+__global__ void __launch_bounds__(256, 2) render_ap_fast(RenderParams p) {
+  static_assert(VB * FY_T <= 256, "one row-factor copy per thread");
+  constexpr int XPT = (VB * FX_T + 255) / 256;  // column-factor copies per thread
+  struct __align__(16) Slot {
+    AxisFactor fx[VB][FX_T];
+    AxisFactor fy[VB][FY_T];
+    float2 L[C][256];
+  };
+  __shared__ Slot S[NSTAGE];
+  const int tid = threadIdx.x;
+  const int lx = fast_col(tid), ly = fast_row(tid);
+  const int kx = blockIdx.y * FX_T + lx, ky = blockIdx.z * FY_T + ly;
+  const int v0 = blockIdx.x * VB;
+  const int nv = min(VB, p.V - v0);
+  const long long Q = (long long)p.Hp * p.Whp;
+  const bool inside = kx < p.Whp && ky < p.Hp;
+  const long long q = inside ? (long long)ky * p.Whp + kx : 0;
+  const float4* DQ = p.dquad;
+  const int zero = p.dq_zero;
+
+  const char* xsrc[XPT];
+  int xdst[XPT];
+  bool xok[XPT], xact[XPT];
+#pragma unroll
+  for (int i = 0; i < XPT; ++i) {
+    const int e = tid + 256 * i;
+    const int b = e / FX_T, c = e % FX_T, col = blockIdx.y * FX_T + c;
+    xact[i] = e < VB * FX_T;
+    xok[i] = xact[i] && b < nv && col < p.Whp;
+    xsrc[i] = reinterpret_cast<const char*>(p.px + (xok[i] ? (size_t)(v0 + b) * p.n * p.Whp + col : 0));
+    xdst[i] = (int)((char*)&S[0].fx[b % VB][c] - (char*)&S[0]);
+  }
+  const long long xstep = (long long)p.Whp * 16;
+  const int yb = tid / FY_T, yr = tid % FY_T, row = blockIdx.z * FY_T + yr;
+  const bool yact = tid < VB * FY_T;
+  const bool yok = yact && yb < nv && row < p.Hp;
+  const char* ysrc = reinterpret_cast<const char*>(p.py + (yok ? (size_t)(v0 + yb) * p.n * p.Hp + row : 0));
+  const long long ystep = (long long)p.Hp * 16;
+  const int ydst = (int)((char*)&S[0].fy[yb % VB][yr] - (char*)&S[0]);
+  const float2* lsrc0 = p.layers + q;
+  const long long lstep = inside ? (long long)C * Q : 0;
+
+  // out-of-grid columns / rows / missing views: zero-filled factors (idx 0 is a
+  // valid entry; their weight is 0 through the zero phase)
+  auto stage = [&](int k) {
+    char* base = reinterpret_cast<char*>(&S[k % NSTAGE]);
+#pragma unroll
+    for (int i = 0; i < XPT; ++i)
+      if (xact[i]) cp_async16(base + xdst[i], xsrc[i] + (xok[i] ? k * xstep : 0), xok[i]);
+    if (yact) cp_async16(base + ydst, ysrc + (yok ? k * ystep : 0), yok);
+    const float2* ls = lsrc0 + k * lstep;
+#pragma unroll
+    for (int c = 0; c < C; ++c) cp_async8(&S[k % NSTAGE].L[c][tid], ls + c * Q, inside);
+    cp_async_commit();
+  };
+
+  u64 acc[VB][C];
+#pragma unroll
+  for (int b = 0; b < VB; ++b)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[b][c] = 0ull;
+  float4 Tn[VB];
+  stage(0);
+  if (p.n > 1) stage(1);
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < VB; ++b) Tn[b] = __ldg(DQ + min(S[0].fx[b][lx].idx + S[0].fy[b][ly].idx, zero));
+  for (int k = 0; k < p.n; ++k) {
+    const Slot& sl = S[k % NSTAGE];
+    const Slot& sn = S[(k + 1) % NSTAGE];
+    if (k > 0) {
+      cp_async_wait<0>();  // layer k + 1 staged (issued one layer ago)
+      __syncthreads();     // ... visible; everyone is done with layer k - 1's slot
+    }
+    if (k + 2 < p.n) stage(k + 2);
+    float2 L[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) L[c] = sl.L[c][tid];
+    const bool more = k + 1 < p.n;
+#pragma unroll
+    for (int b = 0; b < VB; ++b) {
+      const AxisFactor x = sl.fx[b][lx];
+      const AxisFactor y = sl.fy[b][ly];
+      const float4 T = Tn[b];
+      // the quad of (view b, layer k + 1): a whole layer of latency cover
+      if (more) Tn[b] = __ldg(DQ + min(sn.fx[b][lx].idx + sn.fy[b][ly].idx, zero));
+      u64 ab = pack2(T.x, T.y);
+      ffma2s(ab, pack2(T.z, T.w), y.frac);
+      const float2 AB = as_f2(ab);
+      const float s = fmaf(x.frac, AB.y, AB.x);
+      const u64 w = fmul2s(cmul2(make_float2(x.re, x.im), make_float2(y.re, y.im)), s);
+#pragma unroll
+      for (int c = 0; c < C; ++c) cmac_w(acc[b][c], w, L[c]);
+    }
+  }
+  if (!inside) return;
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    if (b >= nv) break;
+#pragma unroll
+    for (int c = 0; c < C; ++c) p.out[((size_t)(v0 + b) * C + c) * Q + q] = as_f2(acc[b][c]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pinhole Horner tile.  With shifts affine in the layer index the weight of
+// layer k at a bin is w_k = w_k0 * z^(k - k0), z = exp(2 pi i (alpha wx + beta wy)),
+// so each block of HB layers is evaluated by Horner's rule
+//     H = (...(L_{k0+HB-1} z + L_{k0+HB-2}) z + ...) z + L_k0       (2 FFMA2 / step)
+// and out += w_k0 * H with the exact block weight w_k0 = px_k0 * py_k0 (the
+// staged factors of the block's first layer).  One thread = one bin x one
+// channel x VB views; no per-layer shared-memory traffic and no per-layer
+// barrier: the layer value is the only per-layer load (prefetched 4 ahead).
+// Phase error of a term: < HB fp32 roundings of z (~5e-7 rad at HB = 8).
+// Nyquist lines (cosine phases, construct.py:68-80) are recomputed directly
+// by render_nyquist_fix.
+// ---------------------------------------------------------------------------
+constexpr int HB = 8;
+
+__global__ void render_z_kernel(RenderParams p) {
+  const int v = blockIdx.x;
+  const double a = p.h_alpha[v], b = p.h_beta[v];
+  for (int kx = threadIdx.x; kx < p.Whp; kx += blockDim.x) {
+    cd ph = axis_phase(a, omega_x_label(kx, p.Wp), false);
+    p.zx[(size_t)v * p.Whp + kx] = make_double2(ph.re, ph.im);
+  }
+  for (int ky = threadIdx.x; ky < p.Hp; ky += blockDim.x) {
+    cd ph = axis_phase(b, omega_y_label(ky, p.Hp), false);
+    p.zy[(size_t)v * p.Hp + ky] = make_double2(ph.re, ph.im);
+  }
+}
+
+// H = H * z + L   (packed: (zr Hr + Lr, zi Hr + Li) then + (-zi Hi, zr Hi))
+__device__ __forceinline__ u64 horner_step(u64 H, u64 z, float2 L) {
+  const float2 h = as_f2(H);
+  u64 t = pack2(L.x, L.y);
+  ffma2s(t, z, h.x);
+  return ffma2_i(t, z, h.y);
+}
+
+template <int VB, int TY, int MINB>
+__global__ void __launch_bounds__(32 * TY, MINB) render_horner(RenderParams p) {
+  constexpr int NP = VB / 2, NT = 32 * TY;
+  static_assert(HB == 8, "the prefetch walk assumes 8-layer blocks");
+  __shared__ __align__(16) float4 WX[2][NP][32];
+  __shared__ __align__(16) float4 WY[2][NP][TY];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, tid = threadIdx.x;
+  const int row0 = blockIdx.z * TY;
+  const int kx = blockIdx.y * 32 + tx, ky = row0 + ty;
+  const int v0 = blockIdx.x * VB;
+  const int nv = min(VB, p.V - v0);
+  const int npairs = (nv + 1) / 2;
+  const long long Q = (long long)p.Hp * p.Whp;
+  const bool inside = kx < p.Whp && ky < p.Hp;
+  const long long q = inside ? (long long)ky * p.Whp + kx : 0;
+
+  // block-weight staging (layer k0 of each block), zero-filled outside
+  const float4* PXG = reinterpret_cast<const float4*>(p.px);
+  const float4* PYG = reinterpret_cast<const float4*>(p.py);
+  auto stage = [&](int blk, int slot) {
+    const size_t k0 = (size_t)blk * HB;
+    for (int e = tid; e < NP * (32 + TY); e += NT) {
+      if (e < NP * 32) {
+        const int pr = e >> 5, cc = e & 31, col = blockIdx.y * 32 + cc;
+        const bool ok = pr < npairs && col < p.Whp;
+        cp_async16(&WX[slot][pr][cc], ok ? PXG + ((size_t)(v0 / 2 + pr) * p.n + k0) * p.Whp + col : PXG, ok);
+      } else {
+        const int e2 = e - NP * 32, pr = e2 / TY, r = e2 % TY, row = row0 + r;
+        const bool ok = pr < npairs && row < p.Hp;
+        cp_async16(&WY[slot][pr][r], ok ? PYG + ((size_t)(v0 / 2 + pr) * p.n + k0) * p.Hp + row : PYG, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  const int nblk = (p.n + HB - 1) / HB;
+  const int nsteps = nblk * p.C;  // (channel, block) pairs, channel-major
+  stage(0, 0);
+
+  // per-view Horner ratio, fp64 product rounded once (reused for every channel)
+  u64 z[VB];
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    z[b] = 0ull;
+    if (inside && b < nv) {
+      const double2 a = p.zx[(size_t)(v0 + b) * p.Whp + kx];
+      const double2 e = p.zy[(size_t)(v0 + b) * p.Hp + ky];
+      // explicit roundings: the same bits whatever slot b the view occupies
+      z[b] = pack2(__double2float_rn(__dsub_rn(__dmul_rn(a.x, e.x), __dmul_rn(a.y, e.y))),
+                   __double2float_rn(__dadd_rn(__dmul_rn(a.x, e.y), __dmul_rn(a.y, e.x))));
+    }
+  }
+
+  // layer stream in processing order: (channel c, block blk, step j) -> layer
+  // blk*HB + HB-1-j of channel c.  Step j consumes R[j & 3] and refills it with
+  // step j + 4: layers k0+3..k0 (j < 4), then the top four of the next block
+  // (of this channel, or block 0 of the next channel), walked with byte pointers.
+  const char* lbase = reinterpret_cast<const char*>(p.layers + q);
+  const long long lsb = (long long)p.C * Q * (long long)sizeof(float2);
+  const long long csb = Q * (long long)sizeof(float2);
+  auto ld_if = [&](const char* ptr, bool ok) -> float2 {
+    return ok ? ld_stream(reinterpret_cast<const float2*>(ptr)) : make_float2(0.f, 0.f);
+  };
+  float2 R[4];
+  {
+    const char* pt = lbase + 7 * lsb;
+#pragma unroll
+    for (int j = 0; j < 4; ++j, pt -= lsb) R[j] = ld_if(pt, 7 - j < p.n);
+  }
+  u64 out[VB], H[VB];
+#pragma unroll
+  for (int b = 0; b < VB; ++b) out[b] = 0ull;
+  int c = 0, blk = 0;
+  for (int st = 0; st < nsteps; ++st) {
+    cp_async_wait<0>();
+    __syncthreads();  // weights of this block visible; the other slot is free
+    // next (channel, block)
+    const int nb = (blk + 1 < nblk) ? blk + 1 : 0;
+    const int nc = (blk + 1 < nblk) ? c : c + 1;
+    if (st + 1 < nsteps) stage(nb, (st + 1) & 1);
+    const int k0 = blk * HB;
+    const char* pa = lbase + c * csb + (k0 + 3) * lsb;
+    const char* pn = lbase + nc * csb + (nb * HB + 7) * lsb;
+    const bool nok = nc < p.C;
+#pragma unroll
+    for (int j = 0; j < HB; ++j) {
+      const float2 L = R[j & 3];
+      if (j < 4) {
+        R[j & 3] = ld_if(pa, k0 + 3 - j < p.n);
+        pa -= lsb;
+      } else {
+        R[j & 3] = ld_if(pn, nok && nb * HB + 7 - (j - 4) < p.n);
+        pn -= lsb;
+      }
+      if (j == 0) {
+#pragma unroll
+        for (int b = 0; b < VB; ++b) H[b] = pack2(L.x, L.y);
+      } else {
+#pragma unroll
+        for (int b = 0; b < VB; ++b) H[b] = horner_step(H[b], z[b], L);
+      }
+    }
+    const int s = st & 1;
+#pragma unroll
+    for (int pr = 0; pr < NP; ++pr) {
+      const float4 x = WX[s][pr][tx];
+      const float4 y = WY[s][pr][ty];
+      const u64 w0 = cmul2(make_float2(x.x, x.y), make_float2(y.x, y.y));
+      const u64 w1 = cmul2(make_float2(x.z, x.w), make_float2(y.z, y.w));
+      cmac_w(out[2 * pr], w0, as_f2(H[2 * pr]));
+      cmac_w(out[2 * pr + 1], w1, as_f2(H[2 * pr + 1]));
+    }
+    if (blk + 1 == nblk) {  // channel c done
+      if (inside) {
+#pragma unroll
+        for (int b = 0; b < VB; ++b)
+          if (b < nv) p.out[((size_t)(v0 + b) * p.C + c) * Q + q] = as_f2(out[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < VB; ++b) out[b] = 0ull;
+    }
+    blk = nb;
+    c = nc;
+  }
+}
+
+// Direct sums on the self-conjugate Nyquist column / row (cosine phases), which
+// the Horner recurrence does not model.
+__global__ void render_nyquist_fix(RenderParams p) {
+  const int ncol = (p.Wp % 2 == 0) ? p.Hp : 0;   // kx = Wp/2, every row
+  const int nrow = (p.Hp % 2 == 0) ? p.Whp : 0;  // ky = Hp/2, every column
+  const long long per_view = (long long)(ncol + nrow) * p.C;
+  const long long total = per_view * p.V;
+  const long long Q = (long long)p.Hp * p.Whp;
+  const float2* PX2 = reinterpret_cast<const float2*>(p.px);
+  const float2* PY2 = reinterpret_cast<const float2*>(p.py);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(e / per_view);
+    const long long r = e % per_view;
+    const int c = (int)(r % p.C);
+    const int i = (int)(r / p.C);
+    const int kx = i < ncol ? p.Wp / 2 : i - ncol;
+    const int ky = i < ncol ? i : p.Hp / 2;
+    const long long q = (long long)ky * p.Whp + kx;
+    float accr = 0.f, acci = 0.f;
+    for (int k = 0; k < p.n; ++k) {
+      const float2 fx = PX2[(((size_t)(v >> 1) * p.n + k) * p.Whp + kx) * 2 + (v & 1)];
+      const float2 fy = PY2[(((size_t)(v >> 1) * p.n + k) * p.Hp + ky) * 2 + (v & 1)];
+      const float wr = fy.x * fx.x - fy.y * fx.y, wi = fy.x * fx.y + fy.y * fx.x;
+      const float2 L = p.layers[((size_t)k * p.C + c) * Q + q];
+      accr = fmaf(wr, L.x, fmaf(-wi, L.y, accr));
+      acci = fmaf(wr, L.y, fmaf(wi, L.x, acci));
+    }
+    p.out[((size_t)v * p.C + c) * Q + q] = make_float2(accr, acci);
+  }
+}
+
+int horner_cfg_env() {
+  const char* e = getenv("FDL_HORNER_CFG");
+  return e ? atoi(e) : 0;
+}
+
+int launch_horner(const RenderParams& p, cudaStream_t st) {
+  render_z_kernel<<<p.V, 256, 0, st>>>(p);
+  FDL_LAUNCH_CHECK("render_z_kernel");
+  // (views per thread, rows per CTA, CTAs per SM): register budget 65536 / (32 TY MINB)
+  const int cfg = getenv("FDL_HORNER_CFG") ? horner_cfg_env() : 1;
+  const int VB = cfg == 1 ? 8 : cfg == 2 ? 24 : cfg == 4 ? 12 : 16;
+  const int TY = (cfg == 1 || cfg == 3) ? 8 : 4;
+  const int rowtiles = (p.Hp + TY - 1) / TY;
+  dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((p.Whp + 31) / 32), (unsigned)rowtiles);
+  switch (cfg) {
+    case 1: render_horner<8, 8, 2><<<grid, 256, 0, st>>>(p); break;
+    case 2: render_horner<24, 4, 2><<<grid, 128, 0, st>>>(p); break;
+    case 3: render_horner<16, 8, 1><<<grid, 256, 0, st>>>(p); break;
+    case 4: render_horner<12, 4, 3><<<grid, 128, 0, st>>>(p); break;
+    default: render_horner<16, 4, 3><<<grid, 128, 0, st>>>(p); break;
+  }
+  FDL_LAUNCH_CHECK("render_horner");
+  if ((p.Wp % 2 == 0) || (p.Hp % 2 == 0)) {
+    const long long total = (long long)p.V * p.C * (p.Hp + p.Whp);
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+    render_nyquist_fix<<<std::max(blocks, 1), 256, 0, st>>>(p);
+    FDL_LAUNCH_CHECK("render_nyquist_fix");
+  }
+  return FDL_OK;
+}
+
 template <int C, int VB>
 void launch_ap(const RenderParams& p, dim3 grid, dim3 block, cudaStream_t st) {
   if (p.uniform_ap >= 0)  // every view on one real table
@@ -338,8 +830,37 @@ int render_vb_env(bool aperture) {
   return aperture ? 8 : 16;
 }
 
+// fast tiles: views per CTA by channel count (accumulators VB * C complex)
+template <int C> struct FastVB;
+template <> struct FastVB<1> { static constexpr int pin = 32, ap = 12; };
+template <> struct FastVB<2> { static constexpr int pin = 24, ap = 8; };
+template <> struct FastVB<3> { static constexpr int pin = 16, ap = 8; };
+template <> struct FastVB<4> { static constexpr int pin = 10, ap = 4; };
+
+bool legacy_render_env() {
+  const char* e = getenv("FDL_RENDER_KERNEL");
+  return e && e[0] == 'l';  // "legacy": the round-1 tile kernels (A/B)
+}
+
 template <int C>
 int launch_sum(const RenderParams& p, cudaStream_t st) {
+  // Horner tile for single-channel pinhole batches (C3: 1.05 vs 1.40 ms for
+  // 81 views); with C >= 2 the direct tile shares each weight across the
+  // channels and wins (C2: 0.92 vs 1.08 ms).  FDL_RENDER_KERNEL=horner|fast|legacy overrides.
+  const char* rk = getenv("FDL_RENDER_KERNEL");
+  const bool want_horner = rk ? rk[0] == 'h' : C == 1;
+  if (p.horner && p.view_ap == nullptr && want_horner) return launch_horner(p, st);
+  if (!legacy_render_env() && (p.view_ap == nullptr || p.fast_ap)) {
+    const bool ap = p.view_ap != nullptr;
+    const int VB = ap ? FastVB<C>::ap : FastVB<C>::pin;
+    dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((p.Whp + FX_T - 1) / FX_T), (unsigned)((p.Hp + FY_T - 1) / FY_T));
+    if (ap)
+      render_ap_fast<C, FastVB<C>::ap><<<grid, 256, 0, st>>>(p);
+    else
+      render_pin_fast<C, FastVB<C>::pin><<<grid, 256, 0, st>>>(p);
+    FDL_LAUNCH_CHECK("render_fast_kernel");
+    return FDL_OK;
+  }
   constexpr int VB = C <= 3 ? 16 : 8;
   dim3 block(TX, TY);
   // view blocks vary fastest: the CTAs that share a layer tile run together and

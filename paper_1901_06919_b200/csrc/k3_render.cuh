@@ -20,7 +20,7 @@ struct RenderTable {
 };
 
 struct RenderParams {
-  int uniform_ap;          // >= 0: every view of the batch uses this real table (fast path)
+  int uniform_ap;         // >= 0: every view of the batch uses this real table (fast path)
   int n, C, Hp, Wp, Whp, V;
   const double* pu;        // (V, n)
   const double* pv;        // (V, n)
@@ -33,6 +33,24 @@ struct RenderParams {
   long long* oob;          // (V) or nullptr
   AxisFactor* px;          // (V, n, Whp)
   AxisFactor* py;          // (V, n, Hp)
+  // real-table fast path (every aperture of the batch real; pinhole views allowed):
+  // difference-form quads (a, b, c, d) = (T00, T01-T00, T10-T00, T11-T10-T01+T00)
+  // so psi = (a + fy c) + fx (b + fy d); tables concatenated, then the ONE entry
+  // (1,0,0,0) that non-aperture views point at and the ZERO entry that
+  // out-of-range lookups point at.  Factor idx fields are absolute entry indices
+  // (x: table base + column, y: row * cols; either axis out of range: dq_zero).
+  int fast_ap;
+  const float4* dquad;
+  const int* ap_qbase;     // (n_apertures) first entry of each table in dquad
+  int dq_one, dq_zero;
+  // pinhole Horner path (every view's shifts affine in the layer index:
+  // pu[v, k] = pu[v, 0] + k * alpha_v, pv likewise): per-bin ratio of
+  // consecutive layer phases z = exp(2 pi i (alpha wx + beta wy)), fp64 tables
+  int horner;
+  const double* h_alpha;   // (V)
+  const double* h_beta;    // (V)
+  double2* zx;             // (V, Whp)
+  double2* zy;             // (V, Hp)
 };
 
 int render_launch(const RenderParams& p, cudaStream_t st);

@@ -264,9 +264,10 @@ def render_many_device(model: FdlModel, reqs, batch: int = 64, timing=None, on_b
     n, C = layers.shape[0], layers.shape[1]
     out = torch.empty((len(reqs), Ho, Wo, C), dtype=torch.float32, device=layers.device)
     oob = torch.zeros((len(reqs),), dtype=torch.int64, device=layers.device)
-    for b0 in range(0, len(reqs), batch):
-        chunk = reqs[b0:b0 + batch]
+    for idx in _kernel_groups(reqs, batch):
+        chunk = [reqs[i] for i in idx]
         V = len(chunk)
+        contiguous = idx[-1] - idx[0] == V - 1
         u = np.array([r.u for r in chunk], dtype=np.float64)
         v = np.array([r.v for r in chunk], dtype=np.float64)
         pu = u[:, None] * d[None, :]
@@ -287,23 +288,51 @@ def render_many_device(model: FdlModel, reqs, batch: int = 64, timing=None, on_b
         if timing is not None:
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             evs[0].record()
+        c_oob = oob[idx[0]:idx[0] + V] if contiguous else torch.zeros((V,), dtype=torch.int64, device=layers.device)
         spec = render_spectra_batch(layers, d, Hp, Wp, pu, pv, t=t,
-                                    view_ap=view_ap if aps else None, apertures=aps, oob=oob[b0:b0 + V])
+                                    view_ap=view_ap if aps else None, apertures=aps, oob=c_oob)
         if evs is not None:
             evs[1].record()
-        flags = srgb[b0:b0 + V]
+        flags = [srgb[i] for i in idx]
         if all(flags) or not any(flags):
-            out[b0:b0 + V] = spectra_to_images(spec, Hp, Wp, pad, Ho, Wo, srgb=flags[0])
+            imgs = spectra_to_images(spec, Hp, Wp, pad, Ho, Wo, srgb=flags[0])
         else:
-            for i in range(V):
-                out[b0 + i:b0 + i + 1] = spectra_to_images(spec[i:i + 1].contiguous(), Hp, Wp, pad, Ho, Wo,
-                                                           srgb=flags[i])
+            imgs = torch.cat([spectra_to_images(spec[i:i + 1].contiguous(), Hp, Wp, pad, Ho, Wo, srgb=flags[i])
+                              for i in range(V)])
         if evs is not None:
             evs[2].record()
             timing.append(evs)
-        if on_batch is not None:
-            on_batch(b0, V, out[b0:b0 + V])
+        if contiguous:
+            out[idx[0]:idx[0] + V] = imgs
+            if on_batch is not None:
+                on_batch(idx[0], V, out[idx[0]:idx[0] + V])
+        else:
+            it = torch.as_tensor(idx, device=layers.device)
+            out.index_copy_(0, it, imgs)
+            oob.index_copy_(0, it, c_oob)
+            if on_batch is not None:
+                for i in idx:
+                    on_batch(i, 1, out[i:i + 1])
     return out, oob
+
+
+def _kernel_groups(reqs, batch):
+    """Request indices in K3 launches of <= `batch` views.  Views are grouped by
+    the render tile they need (pinhole / real aperture table / complex table),
+    so a view's image never depends on which other views share its launch
+    (render_many(...)[i] == render(reqs[i]) bit for bit)."""
+    def kind(r):
+        if not _uses_aperture(r):
+            return 0
+        return 2 if np.iscomplexobj(r.aperture.table) else 1
+    kinds = [kind(r) for r in reqs]
+    if len(set(kinds)) == 1:
+        return [list(range(b0, min(b0 + batch, len(reqs)))) for b0 in range(0, len(reqs), batch)]
+    groups = []
+    for k in sorted(set(kinds)):
+        members = [i for i, kk in enumerate(kinds) if kk == k]
+        groups += [members[b0:b0 + batch] for b0 in range(0, len(members), batch)]
+    return groups
 
 
 def _to_numpy_images(imgs, dtype=np.float64):

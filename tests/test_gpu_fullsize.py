@@ -160,3 +160,21 @@ def test_c5_full_size_renders(fdl):
         assert p >= 60.0
         assert fdl.last_render_stats().oob_lookups == st["oob_lookups"]
     del torch
+
+
+def test_c5_layers_pinhole_renders(fdl):
+    """64-layer pinhole renders (the Horner tile: 8-layer blocks, fp32 ratio z)
+    at full 1920x1080 size, both Nyquist lines present, vs the oracle."""
+    from harness.synth import random_fdl_layers
+    n, C, H, W = 64, 3, 1080, 1920
+    layers = random_fdl_layers(n, C, H, W, device="cuda")
+    d = np.linspace(-5, 5, n)
+    model = fdl.FdlModel(disparities=d, layers=layers, grid=fdl.FrequencyGrid(W, H), width=W, height=H)
+    L = layers.cpu().numpy().astype(np.complex128)
+    uv = [(0.0, 0.0), (4.0, -4.0), (-2.7, 3.9), (0.37, -1.21)]
+    imgs = fdl.render_many(model, [fdl.RenderRequest(u=u, v=v) for u, v in uv])
+    for (u, v), img in zip(uv, imgs):
+        ref, _ = O.render(L, d, H, W, 0, H, W, u=u, v=v)
+        p = psnr(img, ref)
+        print(f"C5-layer pinhole render ({u},{v}): {p:.1f} dB")
+        assert p >= 60.0
