@@ -39,6 +39,17 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 FP64_PEAK_TFLOPS = 36.88  # DMMA m8n8k4 measured on this pool's B200 (profiles/r01_fp64_pipes.txt)
+FP32_PEAK_TFLOPS = 73.45  # FFMA2 (fma.rn.f32x2) measured on this pool's B200 (profiles/r01_fp32_pipes.txt)
+
+
+def render_roofline(flops_per_view: float, views: int, k3_s: float, kernel: str) -> dict:
+    """K3 against the FP32 pipe (8C + 6 (+8 with an aperture)
+    flops per (view, bin, layer)); k3_s = K3 seconds (factor pre-pass + tile)."""
+    achieved = flops_per_view * views / k3_s / 1e12 if k3_s > 0 else None
+    return {"bound": "fp32", "kernel": kernel, "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS if achieved else None,
+            "flops_per_view": flops_per_view, "k3_ms": 1e3 * k3_s,
+            "peak_source": "measured FFMA2 (tools/microbench/fp32_pipes.cu); MEASURED_PEAKS.json has no fp32 entry"}
 TRAFFIC_FILE = ROOT / "profiles" / "k1_traffic.json"  # dram bytes per K1 launch from `ncu --set full`
 
 
@@ -165,9 +176,10 @@ def run_c5(args, rank, world, device):
     sampler.start()
     torch.cuda.nvtx.range_push("timed")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rtim = []
     e0.record(stream)
     for _ in range(args.steps):
-        R.render_many_device(model, mine, batch=args.batch)
+        R.render_many_device(model, mine, batch=args.batch, timing=rtim)
     e1.record(stream)
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
@@ -179,6 +191,8 @@ def run_c5(args, rank, world, device):
         t = float(tt.item())
     Q = H * (W // 2 + 1)
     flops_view = Q * n * (8 * C + 6 + 8)
+    k3_s = sum(ev[0].elapsed_time(ev[1]) for ev in rtim) / 1e3 / args.steps
+    k4_s = sum(ev[1].elapsed_time(ev[2]) for ev in rtim) / 1e3 / args.steps
     return {"metric": "rendered views/s (config 5)", "value": world * per_step / t, "unit": "views/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 render",
@@ -186,6 +200,8 @@ def run_c5(args, rank, world, device):
             "config": {"workload": f"c5: render {per_step} views/rank of a {n}-layer {W}x{H}x{C} FDL, disk(1) f=2r",
                        "views_per_step": per_step * world},
             "render_flops_tf": flops_view * per_step / t / 1e12,
+            "stages_ms": {"k3_render_spectra_ms": 1e3 * k3_s, "k4_c2r_crop_ms": 1e3 * k4_s},
+            "roofline": render_roofline(flops_view, per_step, k3_s, "K3 render tile (disk aperture, fp32 FFMA2)"),
             "clocks": clocks, "gpu_launches": args.steps * 4 * math.ceil(per_step / args.batch)}
 
 
@@ -323,7 +339,10 @@ def run_ours(args, rank, world, device):
                                    if world > 1 else "1 GPU"),
                    "l2": "inputs (views, spectra, layers) exceed the 126 MB L2; no explicit flush",
                    "k1_path": int(path)},
-        "render": {"value": V / t_ren_mean, "unit": "views/s", "ms": 1e3 * t_ren_mean},
+        "render": {"value": V / t_ren_mean, "unit": "views/s", "ms": 1e3 * t_ren_mean,
+                   "roofline": render_roofline(Q * n * (8 * C + 6), V // world if world > 1 else V,
+                                               stages.get("k3_render_spectra_ms", 0.0) / 1e3,
+                                               "K3 render tile (pinhole, fp32 FFMA2)")},
         "construct_ms": 1e3 * t_con_mean,
         "stages_ms": stages,
         "k1_ms": 1e3 * t_k1_mean,
@@ -336,8 +355,10 @@ def run_ours(args, rank, world, device):
                      "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r01_fp64_pipes.txt); "
                                     "MEASURED_PEAKS.json has no fp64 entry"},
         "clocks": clocks,
+        # per render batch: factor pre-pass + tile + K4 column/row passes (+ z table and
+        # Nyquist fix-up kernels around the single-channel Horner tile)
         "gpu_launches": args.steps * ((6 + world if world > 1 else 6)
-                                      + 4 * math.ceil((V // world + 1 if world > 1 else V) / args.batch)),
+                                      + (6 if C == 1 else 4) * math.ceil((V // world + 1 if world > 1 else V) / args.batch)),
     }
     return res, case, (m, n, C, H, W, pad, Hp, Wp, Q, V)
 

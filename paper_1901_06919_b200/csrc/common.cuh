@@ -163,4 +163,16 @@ __device__ __forceinline__ void cmac2(u64& acc, float wr, float wi, float2 z) {
   ffma2(acc, pack2(z.y, z.x), pack2(-wi, wi));
 }
 
+// asynchronous global -> shared copies (sm_80+ cp.async), zero-filled when !valid
+__device__ __forceinline__ void cpa8(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(gsrc), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cpa16(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gsrc), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
 }  // namespace fdl

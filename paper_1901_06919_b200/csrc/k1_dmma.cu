@@ -206,27 +206,36 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     u_cols = a0.cols;
     u_zero = a0.rows * a0.cols;
   }
+  // The bin's m x C spectra values (one 8-byte word per view plane) and, in
+  // mode 1, its column of phase tables are copied asynchronously: the copy for
+  // bin rep + 1 is issued as soon as bin rep's k-steps have read the buffers,
+  // so it lands under bin rep's factorisation.
+  auto stage_bin = [&](int kxs) {
+    const size_t plane_ = sp_plane(p);
+    const float2* src = p.spectra + sp_boff(p, i, kxs);
+    for (int e = lane; e < p.m * p.C; e += 32) cpa8(&BS[e], src + (size_t)e * plane_, true);
+    if (MODE == MODE_SYMREAL) {
+      const double2* srcx = f.px_all + (size_t)kxs * f.nu * f.hw;
+      for (int e = lane; e < f.nu * f.hw; e += 32) {
+        const int rr = e / f.hw;
+        cpa16(reinterpret_cast<double2*>(PX) + rr * f.hwp + (e - rr * f.hw), srcx + e, true);
+      }
+    }
+    cpa_commit();
+  };
+  {
+    const int kx0 = blockIdx.x * p.reps * WARPS + warp;
+    if (kx0 < p.Whp) stage_bin(kx0);
+  }
   for (int rep = 0; rep < p.reps; ++rep) {
   const int kx = (blockIdx.x * p.reps + rep) * WARPS + warp;
   if (kx >= p.Whp) break;  // warp-uniform
+  const int kx_next = kx + WARPS;
+  const bool has_next = rep + 1 < p.reps && kx_next < p.Whp;
   const double ox = omega_x_label(kx, p.Wp);
   const bool nyq_x = (p.Wp % 2 == 0) && kx == p.Wp / 2;
-  __syncwarp();  // the previous bin's readers of this warp's buffers are done
-
-  {
-    // stage this bin's m x C spectra values (one 8-byte load per view plane, all in flight)
-    const size_t plane_ = sp_plane(p);
-    const float2* src = p.spectra + sp_boff(p, i, kx);
-    for (int e = lane; e < p.m * p.C; e += 32) BS[e] = src[(size_t)e * plane_];
-  }
-  if (MODE == MODE_SYMREAL) {
-    const double2* src = f.px_all + (size_t)kx * f.nu * f.hw;
-    for (int e = lane; e < f.nu * f.hw; e += 32) {
-      const int rr = e / f.hw;
-      reinterpret_cast<double2*>(PX)[rr * f.hwp + (e - rr * f.hw)] = src[e];
-    }
-  }
-  __syncwarp();
+  cpa_wait_all();
+  __syncwarp();  // this bin's staged values visible to the whole warp
 
   double g[NBLK][2];
   double r[NB][2];
@@ -343,6 +352,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
 #pragma unroll kKUnroll
   for (int r0 = 0; r0 < mfull; r0 += 4) kstep(r0, false);
   if (mfull < p.m) kstep(mfull, true);
+  __syncwarp();  // every lane is done with BS / PX of this bin
+  if (has_next) stage_bin(kx_next);
 
   if (MODE == MODE_SYMREAL && th) {
     // RHS columns 6/7 = M^T [Re A_0, Im A_0]  ->  t[r], r = 0..n-1  ->  G fragments

@@ -850,7 +850,10 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
   const char* rk = getenv("FDL_RENDER_KERNEL");
   const bool want_horner = rk ? rk[0] == 'h' : C == 1;
   if (p.horner && p.view_ap == nullptr && want_horner) return launch_horner(p, st);
-  if (!legacy_render_env() && (p.view_ap == nullptr || p.fast_ap)) {
+  // aperture batches: the round-1 tile stays the default until the fast
+  // aperture tile beats it (C5: 4.0k vs 4.4k views/s); FDL_RENDER_KERNEL=fast selects it
+  const bool fast_ap_ok = p.fast_ap && rk && rk[0] == 'f';
+  if (!legacy_render_env() && (p.view_ap == nullptr || fast_ap_ok)) {
     const bool ap = p.view_ap != nullptr;
     const int VB = ap ? FastVB<C>::ap : FastVB<C>::pin;
     dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((p.Whp + FX_T - 1) / FX_T), (unsigned)((p.Hp + FY_T - 1) / FY_T));
