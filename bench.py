@@ -166,9 +166,10 @@ def run_c5(args, rank, world, device):
     ap = fdl.aperture_spectrum("disk", diameter=1.0)
     reqs = [fdl.RenderRequest(u=u[i], v=v[i], s=s[i], f=f[i], aperture=ap) for i in range(len(u))]
     mine = reqs[rank * per_step:(rank + 1) * per_step]
+    dev_batch = max(args.batch, per_step)  # device-resident: one launch set per step
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        R.render_many_device(model, mine, batch=args.batch)
+        R.render_many_device(model, mine, batch=dev_batch)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -179,7 +180,7 @@ def run_c5(args, rank, world, device):
     rtim = []
     e0.record(stream)
     for _ in range(args.steps):
-        R.render_many_device(model, mine, batch=args.batch, timing=rtim)
+        R.render_many_device(model, mine, batch=dev_batch, timing=rtim)
     e1.record(stream)
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
@@ -202,7 +203,7 @@ def run_c5(args, rank, world, device):
             "render_flops_tf": flops_view * per_step / t / 1e12,
             "stages_ms": {"k3_render_spectra_ms": 1e3 * k3_s, "k4_c2r_crop_ms": 1e3 * k4_s},
             "roofline": render_roofline(flops_view, per_step, k3_s, "K3 render tile (disk aperture, fp32 FFMA2)"),
-            "clocks": clocks, "gpu_launches": args.steps * 4 * math.ceil(per_step / args.batch)}
+            "clocks": clocks, "gpu_launches": args.steps * 4 * math.ceil(per_step / dev_batch)}
 
 
 def run_ours(args, rank, world, device):
@@ -264,10 +265,14 @@ def run_ours(args, rank, world, device):
         return fdl.FdlModel(disparities=d, layers=layers, grid=fdl.FrequencyGrid(Wp, Hp), width=W, height=H,
                             pad_margin=pad), path
 
+    # device-resident renders: one K3/K4 launch for the whole view set (the
+    # 64-view batches of render_many exist to overlap the host read-back)
+    dev_batch = max(args.batch, V)
+
     def render_step(model, timing=None):
         if sharded:
-            return R.render_many_device(model, my_reqs, batch=args.batch, timing=timing) if my_reqs else None
-        return R.render_many_device(model, reqs, batch=args.batch, timing=timing)
+            return R.render_many_device(model, my_reqs, batch=dev_batch, timing=timing) if my_reqs else None
+        return R.render_many_device(model, reqs, batch=dev_batch, timing=timing)
 
     for _ in range(args.warmup):
         model, path = construct_step()
@@ -355,10 +360,10 @@ def run_ours(args, rank, world, device):
                      "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r01_fp64_pipes.txt); "
                                     "MEASURED_PEAKS.json has no fp64 entry"},
         "clocks": clocks,
-        # per render batch: factor pre-pass + tile + K4 column/row passes (+ z table and
-        # Nyquist fix-up kernels around the single-channel Horner tile)
-        "gpu_launches": args.steps * ((6 + world if world > 1 else 6)
-                                      + (6 if C == 1 else 4) * math.ceil((V // world + 1 if world > 1 else V) / args.batch)),
+        # per render batch (pinhole, Horner tile): z tables + tile + Nyquist fix-up + K4
+        # column pass + K4 row pass = 5 launches (aperture batches: factor pre-pass + tile + K4 = 4)
+        "gpu_launches": args.steps * ((7 + world if world > 1 else 7)
+                                      + 5 * math.ceil((V // world + 1 if world > 1 else V) / dev_batch)),
     }
     return res, case, (m, n, C, H, W, pad, Hp, Wp, Q, V)
 

@@ -213,6 +213,10 @@ typedef struct fdl_render_desc {
 } fdl_render_desc;
 
 size_t fdl_render_workspace(const fdl_render_desc* desc);
+/* O(1) upper bound of fdl_render_workspace (no scan of the descriptor's arrays):
+ * aperture_entries = sum of rows*cols over the batch's aperture tables. */
+size_t fdl_render_workspace_bound(int32_t n, int32_t C, int32_t Hp, int32_t Wp, int32_t V, int32_t n_apertures,
+                                  int64_t aperture_entries);
 int fdl_render_spectra(const fdl_render_desc* desc, void* workspace_dev, size_t workspace_bytes,
                        void* stream);
 

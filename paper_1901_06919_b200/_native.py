@@ -103,6 +103,7 @@ EXPORTS = {
     "fdl_symmetrize_rows": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 5 + [c_int32_p, ctypes.c_void_p]),
     "fdl_rows_to_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int32] * 5 + [ctypes.c_void_p]),
     "fdl_render_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlRenderDesc)]),
+    "fdl_render_workspace_bound": (ctypes.c_size_t, [ctypes.c_int32] * 6 + [ctypes.c_int64]),
     "fdl_render_spectra": (ctypes.c_int, [ctypes.POINTER(FdlRenderDesc), ctypes.c_void_p,
                                           ctypes.c_size_t, ctypes.c_void_p]),
     "fdl_spectra_to_images_workspace": (ctypes.c_size_t, [ctypes.c_int32] * 4),

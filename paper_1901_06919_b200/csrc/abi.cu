@@ -433,19 +433,18 @@ int plan_render(const fdl_render_desc* D, RenderPlan& P) {
   Blob& B = P.blob;
   P.o_pu = B.add(D->pu, vn * sizeof(double));
   P.o_pv = B.add(D->pv, vn * sizeof(double));
-  std::vector<double> t(vn, 0.0);
   std::vector<int> vap(std::max(V, 1), -1);
   const int nap = D->view_aperture ? D->n_apertures : 0;
+  P.o_t = (size_t)-1;  // pinhole batches carry no aperture scale
   if (D->view_aperture) {
     if (!D->t) return fail(FDL_ERR_INVALID, "aperture renders need t = f (s - d)");
     for (int v = 0; v < V; ++v) {
       vap[v] = D->view_aperture[v];
       if (vap[v] >= nap) return fail(FDL_ERR_INVALID, "aperture index out of range");
     }
-    for (size_t e = 0; e < vn; ++e) t[e] = D->t[e];
-    if (!finite_all(t.data(), vn)) return fail(FDL_ERR_INVALID, "aperture scale must be finite");
+    if (!finite_all(D->t, vn)) return fail(FDL_ERR_INVALID, "aperture scale must be finite");
+    P.o_t = B.add(D->t, vn * sizeof(double));
   }
-  P.o_t = B.add(t.data(), vn * sizeof(double));
   P.o_vap = B.add(vap.data(), vap.size() * sizeof(int));
   P.o_aps = B.reserve(sizeof(DevAperture) * std::max(nap, 1));
   P.o_tabs = B.reserve(sizeof(RenderTable) * std::max(nap, 1));
@@ -552,7 +551,7 @@ size_t render_ws_bytes(const RenderPlan& P) {
   const size_t ve = (size_t)((p.V + 1) & ~1);  // pinhole layout pairs views
   size_t b = P.blob.size() + align256(sizeof(AxisFactor) * ve * p.n * p.Whp) +
              align256(sizeof(AxisFactor) * ve * p.n * p.Hp);
-  if (p.horner) b += align256(sizeof(double2) * ve * p.Whp) + align256(sizeof(double2) * ve * p.Hp);
+  if (p.horner) b += align256(2 * sizeof(double2) * ve * p.Whp) + align256(2 * sizeof(double2) * ve * p.Hp);
   return b;
 }
 
@@ -560,7 +559,7 @@ void bind_render(RenderPlan& P, const fdl_render_desc* D, void* ws) {
   RenderParams& p = P.p;
   p.pu = at<double>(ws, P.o_pu);
   p.pv = at<double>(ws, P.o_pv);
-  p.t = at<double>(ws, P.o_t);
+  p.t = P.o_t == (size_t)-1 ? nullptr : at<double>(ws, P.o_t);
   p.view_ap = D->view_aperture ? at<int>(ws, P.o_vap) : nullptr;
   p.aps = at<DevAperture>(ws, P.o_aps);
   p.tables = at<RenderTable>(ws, P.o_tabs);
@@ -594,7 +593,7 @@ void bind_render(RenderPlan& P, const fdl_render_desc* D, void* ws) {
   if (p.horner) {
     char* zb = base + align256(sizeof(AxisFactor) * ve * p.n * p.Whp) + align256(sizeof(AxisFactor) * ve * p.n * p.Hp);
     p.zx = reinterpret_cast<double2*>(zb);
-    p.zy = reinterpret_cast<double2*>(zb + align256(sizeof(double2) * ve * p.Whp));
+    p.zy = reinterpret_cast<double2*>(zb + align256(2 * sizeof(double2) * ve * p.Whp));
     p.h_alpha = at<double>(ws, P.o_ha);
     p.h_beta = at<double>(ws, P.o_hb);
   }
@@ -889,6 +888,22 @@ size_t fdl_render_workspace(const fdl_render_desc* desc) {
   RenderPlan P;
   if (plan_render(desc, P)) return 0;
   return render_ws_bytes(P);
+}
+
+size_t fdl_render_workspace_bound(int32_t n, int32_t C, int32_t Hp, int32_t Wp, int32_t V, int32_t n_apertures,
+                                  int64_t aperture_entries) {
+  if (n < 1 || C < 1 || Hp < 1 || Wp < 1 || V < 0 || n_apertures < 0 || aperture_entries < 0) return 0;
+  const size_t Whp = (size_t)Wp / 2 + 1, ve = (size_t)((V + 1) & ~1), vn = (size_t)std::max(V, 1) * n;
+  const size_t nap = (size_t)std::max(n_apertures, 1), ent = (size_t)aperture_entries;
+  size_t b = 3 * align256(vn * sizeof(double)) + align256(sizeof(int) * std::max(V, 1));  // pu, pv, t, view map
+  b += align256(sizeof(DevAperture) * nap) + align256(sizeof(RenderTable) * nap);
+  b += 2 * (align256(sizeof(float4) * (ent + nap)) + 256 * nap);           // quad tables (re, im)
+  b += align256(sizeof(float4) * (ent + 2)) + align256(sizeof(int) * nap);  // difference-form tables
+  b += 2 * align256(sizeof(double) * std::max(V, 1));                      // Horner slopes
+  b += 256 * 8;                                                            // alignment slack
+  b += align256(sizeof(AxisFactor) * ve * n * Whp) + align256(sizeof(AxisFactor) * ve * n * Hp);
+  b += align256(2 * sizeof(double2) * ve * Whp) + align256(2 * sizeof(double2) * ve * Hp);
+  return b;
 }
 
 int fdl_render_spectra(const fdl_render_desc* desc, void* workspace_dev, size_t workspace_bytes, void* stream) {

@@ -605,16 +605,26 @@ __global__ void __launch_bounds__(256, 2) render_ap_fast(RenderParams p) {
 // ---------------------------------------------------------------------------
 constexpr int HB = 8;
 
+// fp64 axis tables of the Horner tiles: ratio exp(2 pi i alpha_v wx) at
+// zx[v][kx] and the layer-0 phase exp(2 pi i pu[v,0] wx) at zx[V + v][kx]
+// (rows likewise); cosine lines are not special here (render_nyquist_fix).
 __global__ void render_z_kernel(RenderParams p) {
   const int v = blockIdx.x;
   const double a = p.h_alpha[v], b = p.h_beta[v];
+  const double a0 = p.pu[(size_t)v * p.n], b0 = p.pv[(size_t)v * p.n];
   for (int kx = threadIdx.x; kx < p.Whp; kx += blockDim.x) {
-    cd ph = axis_phase(a, omega_x_label(kx, p.Wp), false);
+    const double ox = omega_x_label(kx, p.Wp);
+    cd ph = axis_phase(a, ox, false);
     p.zx[(size_t)v * p.Whp + kx] = make_double2(ph.re, ph.im);
+    ph = axis_phase(a0, ox, false);
+    p.zx[((size_t)p.V + v) * p.Whp + kx] = make_double2(ph.re, ph.im);
   }
   for (int ky = threadIdx.x; ky < p.Hp; ky += blockDim.x) {
-    cd ph = axis_phase(b, omega_y_label(ky, p.Hp), false);
+    const double oy = omega_y_label(ky, p.Hp);
+    cd ph = axis_phase(b, oy, false);
     p.zy[(size_t)v * p.Hp + ky] = make_double2(ph.re, ph.im);
+    ph = axis_phase(b0, oy, false);
+    p.zy[((size_t)p.V + v) * p.Hp + ky] = make_double2(ph.re, ph.im);
   }
 }
 
@@ -751,35 +761,207 @@ __global__ void __launch_bounds__(32 * TY, MINB) render_horner(RenderParams p) {
   }
 }
 
-// Direct sums on the self-conjugate Nyquist column / row (cosine phases), which
-// the Horner recurrence does not model.
+// ---------------------------------------------------------------------------
+// Single-accumulator Horner tile (all channels of a bin in one thread).
+//   acc <- acc * m_k + L_k   for k = n-1 .. 0,   out = w_0 * acc
+// with m_k = z32 (the fp32-rounded ratio z) except at k = 8b + 7, where
+// m_k = zc = z32 * (z / z32)^8: every 8 steps the drift of the rounded ratio
+// is cancelled, so a term's phase error stays below (7 + n/8) fp32 roundings
+// (< 1e-6 rad at n = 64).  Per (view, bin, layer): C complex multiply-adds
+// (2 FFMA2 each) and nothing else -- no factor traffic, no barrier.  The layer
+// values stream through a per-thread cp.async ring in shared memory (each
+// thread reads only what it copied: no block synchronisation).
+// ---------------------------------------------------------------------------
+constexpr int H2_RING = 8;
+
+template <int C, int VB>
+__global__ void __launch_bounds__(128, 4) render_horner2(RenderParams p) {
+  __shared__ __align__(16) float2 LR[H2_RING][C][128];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int kx = blockIdx.y * 32 + tx, ky = blockIdx.z * 4 + ty;
+  const int v0 = blockIdx.x * VB;
+  const int nv = min(VB, p.V - v0);
+  const long long Q = (long long)p.Hp * p.Whp;
+  const bool inside = kx < p.Whp && ky < p.Hp;
+  const long long q = inside ? (long long)ky * p.Whp + kx : 0;
+  const int n = p.n;
+  const int nb = (n + HB - 1) / HB;
+  const int ktop = nb * HB - 1;  // the stream starts at the (zero-padded) top of the last block
+
+  // layer stream, descending k from ktop; slot s % H2_RING holds step s (layer
+  // ktop - s).  One byte pointer walks down the layers (no per-step multiplies).
+  static_assert(H2_RING == HB, "ring slot = step index within the block");
+  const long long qb = Q * (long long)sizeof(float2);
+  const long long step_b = (long long)C * qb;
+  const char* src = reinterpret_cast<const char*>(p.layers + q) + (long long)ktop * step_b;
+  int k_is = ktop;
+  auto issue = [&](int slot) {
+    const bool ok = inside && k_is < n && k_is >= 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) cp_async8(&LR[slot][c][tid], ok ? src + c * qb : reinterpret_cast<const char*>(p.layers), ok);
+    cp_async_commit();
+    src -= step_b;
+    --k_is;
+  };
+  const int nsteps = nb * HB;
+#pragma unroll
+  for (int s = 0; s < H2_RING - 1; ++s) issue(s);
+
+  // z and the drift-corrected block multiplier zc, from the fp64 axis tables;
+  // explicit roundings: the same bits whatever slot the view occupies
+  u64 z[VB], zc[VB];
+  double2 za[VB], ze[VB];  // all table loads in flight before the fp64 math
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    const bool ok = inside && b < nv;
+    za[b] = ok ? p.zx[(size_t)(v0 + b) * p.Whp + kx] : make_double2(1.0, 0.0);
+    ze[b] = ok ? p.zy[(size_t)(v0 + b) * p.Hp + ky] : make_double2(1.0, 0.0);
+  }
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    z[b] = 0ull;
+    zc[b] = 0ull;
+    if (inside && b < nv) {
+      const double2 a = za[b];
+      const double2 e = ze[b];
+      const double zr = __dsub_rn(__dmul_rn(a.x, e.x), __dmul_rn(a.y, e.y));
+      const double zi = __dadd_rn(__dmul_rn(a.x, e.y), __dmul_rn(a.y, e.x));
+      const float fr = __double2float_rn(zr), fi = __double2float_rn(zi);
+      // r = z / z32 = z * conj(z32) / |z32|^2, then r^8 by three squarings
+      const double n2 = __dadd_rn(__dmul_rn((double)fr, (double)fr), __dmul_rn((double)fi, (double)fi));
+      const double inv_n2 = __dsub_rn(2.0, n2);  // 1/n2 to O((1-n2)^2) ~ 1e-14: |z32| = 1 +- 1e-7
+      double rr = __dmul_rn(__dadd_rn(__dmul_rn(zr, (double)fr), __dmul_rn(zi, (double)fi)), inv_n2);
+      double ri = __dmul_rn(__dsub_rn(__dmul_rn(zi, (double)fr), __dmul_rn(zr, (double)fi)), inv_n2);
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const double sr = __dsub_rn(__dmul_rn(rr, rr), __dmul_rn(ri, ri));
+        const double si = __dmul_rn(2.0, __dmul_rn(rr, ri));
+        rr = sr;
+        ri = si;
+      }
+      z[b] = pack2(fr, fi);
+      zc[b] = pack2(__double2float_rn(__dsub_rn(__dmul_rn((double)fr, rr), __dmul_rn((double)fi, ri))),
+                    __double2float_rn(__dadd_rn(__dmul_rn((double)fr, ri), __dmul_rn((double)fi, rr))));
+    }
+  }
+  u64 acc[VB][C];
+#pragma unroll
+  for (int b = 0; b < VB; ++b)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[b][c] = 0ull;
+
+  for (int blk = 0; blk < nb; ++blk) {
+#pragma unroll
+    for (int j = 0; j < HB; ++j) {
+      const int s = blk * HB + j;  // layer ktop - s = (nb-1-blk)*8 + 7 - j
+      if (s + H2_RING - 1 < nsteps) issue((j + H2_RING - 1) % H2_RING); else cp_async_commit();
+      cp_async_wait<H2_RING - 1>();  // step s landed (this thread's own copies)
+      float2 L[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) L[c] = LR[j][c][tid];
+#pragma unroll
+      for (int b = 0; b < VB; ++b) {
+        const u64 m = (j == 0) ? zc[b] : z[b];
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[b][c] = horner_step(acc[b][c], m, L[c]);
+      }
+    }
+  }
+  if (!inside) return;
+  // out = w_0 * acc, w_0 = exp(2 pi i (pu[v,0] wx + pv[v,0] wy)) from the fp64 tables
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    if (b >= nv) break;
+    const int v = v0 + b;
+    const double2 a = p.zx[((size_t)p.V + v) * p.Whp + kx];
+    const double2 e = p.zy[((size_t)p.V + v) * p.Hp + ky];
+    const u64 w0 = pack2(__double2float_rn(__dsub_rn(__dmul_rn(a.x, e.x), __dmul_rn(a.y, e.y))),
+                         __double2float_rn(__dadd_rn(__dmul_rn(a.x, e.y), __dmul_rn(a.y, e.x))));
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      u64 o = 0ull;
+      cmac_w(o, w0, as_f2(acc[b][c]));
+      p.out[((size_t)v * C + c) * Q + q] = as_f2(o);
+    }
+  }
+}
+
+template <int C> struct H2VB;
+template <> struct H2VB<1> { static constexpr int vb = 12; };
+template <> struct H2VB<2> { static constexpr int vb = 10; };
+template <> struct H2VB<3> { static constexpr int vb = 8; };
+template <> struct H2VB<4> { static constexpr int vb = 6; };
+
+template <int C>
+int launch_horner2(const RenderParams& p, cudaStream_t st) {
+  render_z_kernel<<<p.V, 256, 0, st>>>(p);
+  FDL_LAUNCH_CHECK("render_z_kernel");
+  constexpr int VB = H2VB<C>::vb;
+  dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((p.Whp + 31) / 32), (unsigned)((p.Hp + 3) / 4));
+  render_horner2<C, VB><<<grid, 128, 0, st>>>(p);
+  FDL_LAUNCH_CHECK("render_horner2");
+  return FDL_OK;
+}
+
+// Direct sums on the self-conjugate Nyquist column / row, whose cosine phases
+// (construct.py:68-80) the Horner recurrences do not model.  One thread per
+// (line bin, view), every channel; the per-axis phases run as fp64
+// recurrences from exact start values (shifts are affine on the Horner path):
+// X_k = e^{i pi Pu_k} (cosine line: value Re X_k) or e^{2 pi i Pu_k wx}.
 __global__ void render_nyquist_fix(RenderParams p) {
   const int ncol = (p.Wp % 2 == 0) ? p.Hp : 0;   // kx = Wp/2, every row
   const int nrow = (p.Hp % 2 == 0) ? p.Whp : 0;  // ky = Hp/2, every column
-  const long long per_view = (long long)(ncol + nrow) * p.C;
-  const long long total = per_view * p.V;
+  const int nl = ncol + nrow;
+  const long long total = (long long)nl * p.V * p.C;
   const long long Q = (long long)p.Hp * p.Whp;
-  const float2* PX2 = reinterpret_cast<const float2*>(p.px);
-  const float2* PY2 = reinterpret_cast<const float2*>(p.py);
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-    const int v = (int)(e / per_view);
-    const long long r = e % per_view;
-    const int c = (int)(r % p.C);
-    const int i = (int)(r / p.C);
+    // views fastest: a warp's layer loads are one broadcast address
+    const int v = (int)(e % p.V);
+    const int c = (int)((e / p.V) % p.C), i = (int)(e / p.V / p.C);
     const int kx = i < ncol ? p.Wp / 2 : i - ncol;
     const int ky = i < ncol ? i : p.Hp / 2;
+    if (i >= ncol && kx == p.Wp / 2 && ncol) continue;  // the corner is done by the column entry
+    const bool nx = (p.Wp % 2 == 0) && kx == p.Wp / 2, ny = (p.Hp % 2 == 0) && ky == p.Hp / 2;
+    const double ox = omega_x_label(kx, p.Wp), oy = omega_y_label(ky, p.Hp);
+    const double* pu = p.pu + (size_t)v * p.n;
+    const double* pv = p.pv + (size_t)v * p.n;
+    const double a = p.h_alpha[v], b = p.h_beta[v];
+    // start phases and ratios: cosine lines e^{i pi P}, else e^{2 pi i P w}
+    double sxr, sxi, rxr, rxi, syr, syi, ryr, ryi;
+    sincospi(nx ? pu[0] : 2.0 * pu[0] * ox, &sxi, &sxr);
+    sincospi(nx ? a : 2.0 * a * ox, &rxi, &rxr);
+    sincospi(ny ? pv[0] : 2.0 * pv[0] * oy, &syi, &syr);
+    sincospi(ny ? b : 2.0 * b * oy, &ryi, &ryr);
     const long long q = (long long)ky * p.Whp + kx;
-    float accr = 0.f, acci = 0.f;
+    const float2* lp = p.layers + (size_t)c * Q + q;
+    const long long lstride = (long long)p.C * Q;
+    double accr = 0.0, acci = 0.0;
+#pragma unroll 8
     for (int k = 0; k < p.n; ++k) {
-      const float2 fx = PX2[(((size_t)(v >> 1) * p.n + k) * p.Whp + kx) * 2 + (v & 1)];
-      const float2 fy = PY2[(((size_t)(v >> 1) * p.n + k) * p.Hp + ky) * 2 + (v & 1)];
-      const float wr = fy.x * fx.x - fy.y * fx.y, wi = fy.x * fx.y + fy.y * fx.x;
-      const float2 L = p.layers[((size_t)k * p.C + c) * Q + q];
-      accr = fmaf(wr, L.x, fmaf(-wi, L.y, accr));
-      acci = fmaf(wr, L.y, fmaf(wi, L.x, acci));
+      const double xr = sxr, xi = nx ? 0.0 : sxi, yr = syr, yi = ny ? 0.0 : syi;
+      const double wr = xr * yr - xi * yi, wi = xr * yi + xi * yr;
+      const float2 L = __ldg(lp + k * lstride);
+      accr += wr * L.x - wi * L.y;
+      acci += wr * L.y + wi * L.x;
+      double t = sxr * rxr - sxi * rxi;
+      sxi = sxr * rxi + sxi * rxr;
+      sxr = t;
+      t = syr * ryr - syi * ryi;
+      syi = syr * ryi + syi * ryr;
+      syr = t;
     }
-    p.out[((size_t)v * p.C + c) * Q + q] = make_float2(accr, acci);
+    p.out[((size_t)v * p.C + c) * Q + q] = make_float2((float)accr, (float)acci);
   }
+}
+
+int launch_nyquist_fix(const RenderParams& p, cudaStream_t st) {
+  if ((p.Wp % 2 == 0) || (p.Hp % 2 == 0)) {
+    const long long total = (long long)p.V * p.C * (p.Hp + p.Whp);
+    const int blocks = (int)std::min<long long>((total + 127) / 128, 148LL * 16);
+    render_nyquist_fix<<<std::max(blocks, 1), 128, 0, st>>>(p);
+    FDL_LAUNCH_CHECK("render_nyquist_fix");
+  }
+  return FDL_OK;
 }
 
 int horner_cfg_env() {
@@ -804,13 +986,7 @@ int launch_horner(const RenderParams& p, cudaStream_t st) {
     default: render_horner<16, 4, 3><<<grid, 128, 0, st>>>(p); break;
   }
   FDL_LAUNCH_CHECK("render_horner");
-  if ((p.Wp % 2 == 0) || (p.Hp % 2 == 0)) {
-    const long long total = (long long)p.V * p.C * (p.Hp + p.Whp);
-    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
-    render_nyquist_fix<<<std::max(blocks, 1), 256, 0, st>>>(p);
-    FDL_LAUNCH_CHECK("render_nyquist_fix");
-  }
-  return FDL_OK;
+  return launch_nyquist_fix(p, st);
 }
 
 template <int C, int VB>
@@ -842,13 +1018,24 @@ bool legacy_render_env() {
   return e && e[0] == 'l';  // "legacy": the round-1 tile kernels (A/B)
 }
 
+bool use_horner2(const RenderParams& p) {
+  const char* rk = getenv("FDL_RENDER_KERNEL");
+  return p.horner && p.view_ap == nullptr && (!rk || rk[0] == '2');
+}
+
+
 template <int C>
 int launch_sum(const RenderParams& p, cudaStream_t st) {
   // Horner tile for single-channel pinhole batches (C3: 1.05 vs 1.40 ms for
   // 81 views); with C >= 2 the direct tile shares each weight across the
   // channels and wins (C2: 0.92 vs 1.08 ms).  FDL_RENDER_KERNEL=horner|fast|legacy overrides.
   const char* rk = getenv("FDL_RENDER_KERNEL");
-  const bool want_horner = rk ? rk[0] == 'h' : C == 1;
+  if (use_horner2(p)) {
+    int rc = launch_horner2<C>(p, st);
+    if (rc) return rc;
+    return launch_nyquist_fix(p, st);
+  }
+  const bool want_horner = rk && rk[0] == 'h';
   if (p.horner && p.view_ap == nullptr && want_horner) return launch_horner(p, st);
   // aperture batches: the round-1 tile stays the default until the fast
   // aperture tile beats it (C5: 4.0k vs 4.4k views/s); FDL_RENDER_KERNEL=fast selects it
@@ -887,8 +1074,10 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
 
 int render_launch(const RenderParams& p, cudaStream_t st) {
   if (p.V == 0) return FDL_OK;
-  render_factors_kernel<<<p.V * p.n, 256, 0, st>>>(p);
-  FDL_LAUNCH_CHECK("render_factors_kernel");
+  if (!use_horner2(p)) {  // the Horner tile needs no per-layer factors
+    render_factors_kernel<<<p.V * p.n, 256, 0, st>>>(p);
+    FDL_LAUNCH_CHECK("render_factors_kernel");
+  }
   switch (p.C) {
     case 1: return launch_sum<1>(p, st);
     case 2: return launch_sum<2>(p, st);

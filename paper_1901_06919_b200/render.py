@@ -210,9 +210,12 @@ def render_spectra_batch(layers_dev, d, Hp, Wp, pu, pv, t=None, view_ap=None, ap
     desc.out_dev = out.data_ptr()
     desc.oob_dev = oob.data_ptr() if oob is not None else None
     L = nat.lib()
-    ws_bytes = L.fdl_render_workspace(desc)
+    # O(1) bound (fdl_render_spectra plans the batch once; the exact
+    # fdl_render_workspace would scan it a second time on the host)
+    entries = sum(int(np.asarray(a.table).shape[0]) * int(np.asarray(a.table).shape[1]) for a in apertures)
+    ws_bytes = L.fdl_render_workspace_bound(n, C, Hp, Wp, V, len(apertures), entries)
     if ws_bytes == 0:
-        raise nat.FdlNativeError("fdl_render_workspace: " + L.fdl_last_error().decode())
+        raise nat.FdlNativeError("fdl_render_workspace_bound: invalid render shape")
     ws = nat.workspace(ws_bytes, layers_dev.device)
     nat.check(L.fdl_render_spectra(desc, ws.data_ptr(), ws.numel(), nat.stream_handle(layers_dev.device)),
               "fdl_render_spectra")
