@@ -777,6 +777,7 @@ constexpr int H2_RING = 8;
 template <int C, int VB>
 __global__ void __launch_bounds__(128, 4) render_horner2(RenderParams p) {
   __shared__ __align__(16) float2 LR[H2_RING][C][128];
+  __shared__ __align__(16) u64 ZC[VB][128];  // block multipliers (used once per 8 layers)
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int kx = blockIdx.y * 32 + tx, ky = blockIdx.z * 4 + ty;
   const int v0 = blockIdx.x * VB;
@@ -786,30 +787,30 @@ __global__ void __launch_bounds__(128, 4) render_horner2(RenderParams p) {
   const long long q = inside ? (long long)ky * p.Whp + kx : 0;
   const int n = p.n;
   const int nb = (n + HB - 1) / HB;
-  const int ktop = nb * HB - 1;  // the stream starts at the (zero-padded) top of the last block
 
-  // layer stream, descending k from ktop; slot s % H2_RING holds step s (layer
-  // ktop - s).  One byte pointer walks down the layers (no per-step multiplies).
-  static_assert(H2_RING == HB, "ring slot = step index within the block");
+  // layer stream, k = n-1 .. 0; layer k lives in ring slot k & 7 (= a
+  // compile-time index inside the 8-step blocks below).  One byte pointer
+  // walks down the layers; out-of-grid threads copy zeros from a valid address.
+  static_assert(H2_RING == HB, "ring slot = k mod 8");
   const long long qb = Q * (long long)sizeof(float2);
   const long long step_b = (long long)C * qb;
-  const char* src = reinterpret_cast<const char*>(p.layers + q) + (long long)ktop * step_b;
-  int k_is = ktop;
+  const char* src = reinterpret_cast<const char*>(p.layers + q) + (long long)(n - 1) * step_b;
+  int k_is = n - 1;
   auto issue = [&](int slot) {
-    const bool ok = inside && k_is < n && k_is >= 0;
+    if (k_is >= 0) {
+      const char* a0 = src;
 #pragma unroll
-    for (int c = 0; c < C; ++c) cp_async8(&LR[slot][c][tid], ok ? src + c * qb : reinterpret_cast<const char*>(p.layers), ok);
-    cp_async_commit();
-    src -= step_b;
+      for (int c = 0; c < C; ++c, a0 += qb) cp_async8(&LR[slot][c][tid], a0, inside);
+      src -= step_b;
+    }
     --k_is;
+    cp_async_commit();
   };
-  const int nsteps = nb * HB;
-#pragma unroll
-  for (int s = 0; s < H2_RING - 1; ++s) issue(s);
+  for (int s = 0; s < H2_RING - 1; ++s) issue((n - 1 - s) & 7);
 
   // z and the drift-corrected block multiplier zc, from the fp64 axis tables;
   // explicit roundings: the same bits whatever slot the view occupies
-  u64 z[VB], zc[VB];
+  u64 z[VB];
   double2 za[VB], ze[VB];  // all table loads in flight before the fp64 math
 #pragma unroll
   for (int b = 0; b < VB; ++b) {
@@ -819,30 +820,26 @@ __global__ void __launch_bounds__(128, 4) render_horner2(RenderParams p) {
   }
 #pragma unroll
   for (int b = 0; b < VB; ++b) {
-    z[b] = 0ull;
-    zc[b] = 0ull;
-    if (inside && b < nv) {
-      const double2 a = za[b];
-      const double2 e = ze[b];
-      const double zr = __dsub_rn(__dmul_rn(a.x, e.x), __dmul_rn(a.y, e.y));
-      const double zi = __dadd_rn(__dmul_rn(a.x, e.y), __dmul_rn(a.y, e.x));
-      const float fr = __double2float_rn(zr), fi = __double2float_rn(zi);
-      // r = z / z32 = z * conj(z32) / |z32|^2, then r^8 by three squarings
-      const double n2 = __dadd_rn(__dmul_rn((double)fr, (double)fr), __dmul_rn((double)fi, (double)fi));
-      const double inv_n2 = __dsub_rn(2.0, n2);  // 1/n2 to O((1-n2)^2) ~ 1e-14: |z32| = 1 +- 1e-7
-      double rr = __dmul_rn(__dadd_rn(__dmul_rn(zr, (double)fr), __dmul_rn(zi, (double)fi)), inv_n2);
-      double ri = __dmul_rn(__dsub_rn(__dmul_rn(zi, (double)fr), __dmul_rn(zr, (double)fi)), inv_n2);
+    const double2 a = za[b];
+    const double2 e = ze[b];
+    const double zr = __dsub_rn(__dmul_rn(a.x, e.x), __dmul_rn(a.y, e.y));
+    const double zi = __dadd_rn(__dmul_rn(a.x, e.y), __dmul_rn(a.y, e.x));
+    const float fr = __double2float_rn(zr), fi = __double2float_rn(zi);
+    // r = z / z32 = z * conj(z32) / |z32|^2, then r^8 by three squarings
+    const double n2 = __dadd_rn(__dmul_rn((double)fr, (double)fr), __dmul_rn((double)fi, (double)fi));
+    const double inv_n2 = __dsub_rn(2.0, n2);  // 1/n2 to O((1-n2)^2) ~ 1e-14: |z32| = 1 +- 1e-7
+    double rr = __dmul_rn(__dadd_rn(__dmul_rn(zr, (double)fr), __dmul_rn(zi, (double)fi)), inv_n2);
+    double ri = __dmul_rn(__dsub_rn(__dmul_rn(zi, (double)fr), __dmul_rn(zr, (double)fi)), inv_n2);
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
-        const double sr = __dsub_rn(__dmul_rn(rr, rr), __dmul_rn(ri, ri));
-        const double si = __dmul_rn(2.0, __dmul_rn(rr, ri));
-        rr = sr;
-        ri = si;
-      }
-      z[b] = pack2(fr, fi);
-      zc[b] = pack2(__double2float_rn(__dsub_rn(__dmul_rn((double)fr, rr), __dmul_rn((double)fi, ri))),
-                    __double2float_rn(__dadd_rn(__dmul_rn((double)fr, ri), __dmul_rn((double)fi, rr))));
+    for (int t = 0; t < 3; ++t) {
+      const double sr = __dsub_rn(__dmul_rn(rr, rr), __dmul_rn(ri, ri));
+      const double si = __dmul_rn(2.0, __dmul_rn(rr, ri));
+      rr = sr;
+      ri = si;
     }
+    z[b] = pack2(fr, fi);
+    ZC[b][tid] = pack2(__double2float_rn(__dsub_rn(__dmul_rn((double)fr, rr), __dmul_rn((double)fi, ri))),
+                       __double2float_rn(__dadd_rn(__dmul_rn((double)fr, ri), __dmul_rn((double)fi, rr))));
   }
   u64 acc[VB][C];
 #pragma unroll
@@ -850,18 +847,21 @@ __global__ void __launch_bounds__(128, 4) render_horner2(RenderParams p) {
 #pragma unroll
     for (int c = 0; c < C; ++c) acc[b][c] = 0ull;
 
-  for (int blk = 0; blk < nb; ++blk) {
+  // blocks from the top: layers 8 blk' + 7 - j, blk' = nb-1 .. 0 (the top block
+  // may be partial: its missing layers are skipped, uniformly across the CTA)
+  for (int blk = nb - 1; blk >= 0; --blk) {
 #pragma unroll
     for (int j = 0; j < HB; ++j) {
-      const int s = blk * HB + j;  // layer ktop - s = (nb-1-blk)*8 + 7 - j
-      if (s + H2_RING - 1 < nsteps) issue((j + H2_RING - 1) % H2_RING); else cp_async_commit();
-      cp_async_wait<H2_RING - 1>();  // step s landed (this thread's own copies)
+      const int k = blk * HB + HB - 1 - j;
+      if (k >= n) continue;
+      issue((HB - j) & 7);  // layer k - 7 -> slot (k - 7) & 7 = (k + 1) & 7
+      cp_async_wait<H2_RING - 1>();  // layer k landed (this thread's own copies)
       float2 L[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) L[c] = LR[j][c][tid];
+      for (int c = 0; c < C; ++c) L[c] = LR[HB - 1 - j][c][tid];
 #pragma unroll
       for (int b = 0; b < VB; ++b) {
-        const u64 m = (j == 0) ? zc[b] : z[b];
+        const u64 m = (j == 0) ? ZC[b][tid] : z[b];
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[b][c] = horner_step(acc[b][c], m, L[c]);
       }
@@ -887,10 +887,10 @@ __global__ void __launch_bounds__(128, 4) render_horner2(RenderParams p) {
 }
 
 template <int C> struct H2VB;
-template <> struct H2VB<1> { static constexpr int vb = 12; };
-template <> struct H2VB<2> { static constexpr int vb = 10; };
-template <> struct H2VB<3> { static constexpr int vb = 8; };
-template <> struct H2VB<4> { static constexpr int vb = 6; };
+template <> struct H2VB<1> { static constexpr int vb = 16; };
+template <> struct H2VB<2> { static constexpr int vb = 12; };
+template <> struct H2VB<3> { static constexpr int vb = 10; };
+template <> struct H2VB<4> { static constexpr int vb = 8; };
 
 template <int C>
 int launch_horner2(const RenderParams& p, cudaStream_t st) {
@@ -912,37 +912,39 @@ __global__ void render_nyquist_fix(RenderParams p) {
   const int ncol = (p.Wp % 2 == 0) ? p.Hp : 0;   // kx = Wp/2, every row
   const int nrow = (p.Hp % 2 == 0) ? p.Whp : 0;  // ky = Hp/2, every column
   const int nl = ncol + nrow;
-  const long long total = (long long)nl * p.V * p.C;
+  const long long total = (long long)nl * p.V;
   const long long Q = (long long)p.Hp * p.Whp;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
     // views fastest: a warp's layer loads are one broadcast address
-    const int v = (int)(e % p.V);
-    const int c = (int)((e / p.V) % p.C), i = (int)(e / p.V / p.C);
+    const int v = (int)(e % p.V), i = (int)(e / p.V);
     const int kx = i < ncol ? p.Wp / 2 : i - ncol;
     const int ky = i < ncol ? i : p.Hp / 2;
     if (i >= ncol && kx == p.Wp / 2 && ncol) continue;  // the corner is done by the column entry
     const bool nx = (p.Wp % 2 == 0) && kx == p.Wp / 2, ny = (p.Hp % 2 == 0) && ky == p.Hp / 2;
     const double ox = omega_x_label(kx, p.Wp), oy = omega_y_label(ky, p.Hp);
-    const double* pu = p.pu + (size_t)v * p.n;
-    const double* pv = p.pv + (size_t)v * p.n;
+    const double a0 = p.pu[(size_t)v * p.n], b0 = p.pv[(size_t)v * p.n];
     const double a = p.h_alpha[v], b = p.h_beta[v];
-    // start phases and ratios: cosine lines e^{i pi P}, else e^{2 pi i P w}
+    // start phases and ratios in fp64: cosine lines e^{i pi P}, else e^{2 pi i P w}
     double sxr, sxi, rxr, rxi, syr, syi, ryr, ryi;
-    sincospi(nx ? pu[0] : 2.0 * pu[0] * ox, &sxi, &sxr);
+    sincospi(nx ? a0 : 2.0 * a0 * ox, &sxi, &sxr);
     sincospi(nx ? a : 2.0 * a * ox, &rxi, &rxr);
-    sincospi(ny ? pv[0] : 2.0 * pv[0] * oy, &syi, &syr);
+    sincospi(ny ? b0 : 2.0 * b0 * oy, &syi, &syr);
     sincospi(ny ? b : 2.0 * b * oy, &ryi, &ryr);
     const long long q = (long long)ky * p.Whp + kx;
-    const float2* lp = p.layers + (size_t)c * Q + q;
-    const long long lstride = (long long)p.C * Q;
-    double accr = 0.0, acci = 0.0;
-#pragma unroll 8
+    const float2* lp = p.layers + q;
+    float accr[4] = {0.f, 0.f, 0.f, 0.f}, acci[4] = {0.f, 0.f, 0.f, 0.f};
     for (int k = 0; k < p.n; ++k) {
+      // weight in fp64 (one per view, bin, layer), accumulation in fp32 like the tiles
       const double xr = sxr, xi = nx ? 0.0 : sxi, yr = syr, yi = ny ? 0.0 : syi;
-      const double wr = xr * yr - xi * yi, wi = xr * yi + xi * yr;
-      const float2 L = __ldg(lp + k * lstride);
-      accr += wr * L.x - wi * L.y;
-      acci += wr * L.y + wi * L.x;
+      const float wr = (float)(xr * yr - xi * yi), wi = (float)(xr * yi + xi * yr);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < p.C) {
+          const float2 L = __ldg(lp + ((size_t)k * p.C + c) * Q);
+          accr[c] = fmaf(wr, L.x, fmaf(-wi, L.y, accr[c]));
+          acci[c] = fmaf(wr, L.y, fmaf(wi, L.x, acci[c]));
+        }
+      }
       double t = sxr * rxr - sxi * rxi;
       sxi = sxr * rxi + sxi * rxr;
       sxr = t;
@@ -950,13 +952,15 @@ __global__ void render_nyquist_fix(RenderParams p) {
       syi = syr * ryi + syi * ryr;
       syr = t;
     }
-    p.out[((size_t)v * p.C + c) * Q + q] = make_float2((float)accr, (float)acci);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < p.C) p.out[((size_t)v * p.C + c) * Q + q] = make_float2(accr[c], acci[c]);
   }
 }
 
 int launch_nyquist_fix(const RenderParams& p, cudaStream_t st) {
   if ((p.Wp % 2 == 0) || (p.Hp % 2 == 0)) {
-    const long long total = (long long)p.V * p.C * (p.Hp + p.Whp);
+    const long long total = (long long)p.V * (p.Hp + p.Whp);
     const int blocks = (int)std::min<long long>((total + 127) / 128, 148LL * 16);
     render_nyquist_fix<<<std::max(blocks, 1), 128, 0, st>>>(p);
     FDL_LAUNCH_CHECK("render_nyquist_fix");

@@ -184,7 +184,8 @@ def _uses_aperture(req: RenderRequest) -> bool:
     return req.f > 0 and req.aperture is not None and not req.aperture.is_pinhole
 
 
-def render_spectra_batch(layers_dev, d, Hp, Wp, pu, pv, t=None, view_ap=None, apertures=(), oob=None):
+def render_spectra_batch(layers_dev, d, Hp, Wp, pu, pv, t=None, view_ap=None, apertures=(), oob=None,
+                         start_event=None):
     """K3 over V views -> (V, C, Hp, Whp) complex64 CUDA tensor."""
     import torch
     n, C = layers_dev.shape[0], layers_dev.shape[1]
@@ -217,6 +218,8 @@ def render_spectra_batch(layers_dev, d, Hp, Wp, pu, pv, t=None, view_ap=None, ap
     if ws_bytes == 0:
         raise nat.FdlNativeError("fdl_render_workspace_bound: invalid render shape")
     ws = nat.workspace(ws_bytes, layers_dev.device)
+    if start_event is not None:  # stage timing: device work only, after the Python-side preparation
+        start_event.record()
     nat.check(L.fdl_render_spectra(desc, ws.data_ptr(), ws.numel(), nat.stream_handle(layers_dev.device)),
               "fdl_render_spectra")
     return out
@@ -290,10 +293,10 @@ def render_many_device(model: FdlModel, reqs, batch: int = 64, timing=None, on_b
         evs = None
         if timing is not None:
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            evs[0].record()
         c_oob = oob[idx[0]:idx[0] + V] if contiguous else torch.zeros((V,), dtype=torch.int64, device=layers.device)
         spec = render_spectra_batch(layers, d, Hp, Wp, pu, pv, t=t,
-                                    view_ap=view_ap if aps else None, apertures=aps, oob=c_oob)
+                                    view_ap=view_ap if aps else None, apertures=aps, oob=c_oob,
+                                    start_event=evs[0] if evs else None)
         if evs is not None:
             evs[1].record()
         flags = [srgb[i] for i in idx]
