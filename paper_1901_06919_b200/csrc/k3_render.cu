@@ -933,24 +933,32 @@ __global__ void render_nyquist_fix(RenderParams p) {
     const long long q = (long long)ky * p.Whp + kx;
     const float2* lp = p.layers + q;
     float accr[4] = {0.f, 0.f, 0.f, 0.f}, acci[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int k = 0; k < p.n; ++k) {
-      // weight in fp64 (one per view, bin, layer), accumulation in fp32 like the tiles
-      const double xr = sxr, xi = nx ? 0.0 : sxi, yr = syr, yi = ny ? 0.0 : syi;
-      const float wr = (float)(xr * yr - xi * yi), wi = (float)(xr * yi + xi * yr);
+    const long long cq = Q, kq = (long long)p.C * Q;
+    for (int k0 = 0; k0 < p.n; k0 += 8) {
+      // the layer values of 8 layers in flight before the arithmetic
+      float2 Lb[8][4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c < p.C) {
-          const float2 L = __ldg(lp + ((size_t)k * p.C + c) * Q);
-          accr[c] = fmaf(wr, L.x, fmaf(-wi, L.y, accr[c]));
-          acci[c] = fmaf(wr, L.y, fmaf(wi, L.x, acci[c]));
+      for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          Lb[kk][c] = (c < p.C && k0 + kk < p.n) ? __ldg(lp + (k0 + kk) * kq + c * cq) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        // weight in fp64 (one per view, bin, layer), accumulation in fp32 like the tiles
+        const double xr = sxr, xi = nx ? 0.0 : sxi, yr = syr, yi = ny ? 0.0 : syi;
+        const float wr = (float)(xr * yr - xi * yi), wi = (float)(xr * yi + xi * yr);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          accr[c] = fmaf(wr, Lb[kk][c].x, fmaf(-wi, Lb[kk][c].y, accr[c]));
+          acci[c] = fmaf(wr, Lb[kk][c].y, fmaf(wi, Lb[kk][c].x, acci[c]));
         }
+        double t = sxr * rxr - sxi * rxi;
+        sxi = sxr * rxi + sxi * rxr;
+        sxr = t;
+        t = syr * ryr - syi * ryi;
+        syi = syr * ryi + syi * ryr;
+        syr = t;
       }
-      double t = sxr * rxr - sxi * rxi;
-      sxi = sxr * rxi + sxi * rxr;
-      sxr = t;
-      t = syr * ryr - syi * ryi;
-      syi = syr * ryi + syi * ryr;
-      syr = t;
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c)
