@@ -3,8 +3,9 @@
 Drop-in for the reference package `fdl` on these paths (same names, argument
 meaning and exceptions as fdl/__init__.py:3-98 for everything below); the
 compute runs in hand-written sm_100a CUDA kernels behind a C ABI
-(include/fdl_b200.h, libfdl_b200.so).  Out of scope:
-calibration, pipelines, I/O, CLI, HTTP service, viewer.
+(include/fdl_b200.h, libfdl_b200.so).  FDL1 model files are read and
+written straight from / into device memory (io.py).
+Out of scope: calibration, pipelines, CLI, HTTP service, viewer.
 """
 
 from .spectra import DFT_CONVENTION, FrequencyGrid
@@ -31,6 +32,8 @@ from .render import (
     srgb_decode,
     srgb_encode,
 )
+
+from .io import ModelFormatError, load_model, save_model
 
 __version__ = "0.1.0"
 
@@ -62,5 +65,8 @@ __all__ = [
     "render_views_with_shifts",
     "srgb_decode",
     "srgb_encode",
+    "ModelFormatError",
+    "load_model",
+    "save_model",
     "__version__",
 ]
