@@ -8,6 +8,10 @@ kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
 out = subprocess.run(["ncu", "-i", rep] + kf + ["--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
+# first kernel section only (a report can list the same launch more than once)
+_ks = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+if len(_ks) > 1:
+    rows = rows[:_ks[1]]
 h = rows[1]
 ie, src, ss = h.index("Instructions Executed"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
 cols = ["stall_wait", "stall_short_sb", "stall_long_sb", "stall_barrier", "stall_math", "stall_not_selected",

@@ -10,6 +10,10 @@ units = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
+# first kernel section only (a report can list the same launch more than once)
+_ks = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+if len(_ks) > 1:
+    rows = rows[:_ks[1]]
 h = rows[1]
 ie = h.index("Instructions Executed")
 ss = h.index("Warp Stall Sampling (All Samples)")
