@@ -509,10 +509,10 @@ int plan_render(const fdl_render_desc* D, RenderPlan& P) {
       }
     }
   }
-  // pinhole batch whose shifts are affine in the layer index (factored
-  // u_v * d_k with d an arithmetic progression, as linspace gives) -> Horner tile
+  // shifts affine in the layer index (factored u_v * d_k with d an arithmetic
+  // progression, as linspace gives) -> Horner tiles (pinhole or real apertures)
   p.horner = 0;
-  if (!D->view_aperture && n >= 1) {
+  if (n >= 1) {
     std::vector<double> ha(std::max(V, 1), 0.0), hb(std::max(V, 1), 0.0);
     bool affine = true;
     for (int v = 0; v < V && affine; ++v) {

@@ -55,6 +55,8 @@ __global__ void render_factors_kernel(RenderParams p) {
     }
     if (pin)
       PX2[2 * (size_t)kx] = make_float2(f.re, f.im);
+    else if (p.aux8)
+      reinterpret_cast<float2*>(p.px)[(size_t)vk * p.Whp + kx] = make_float2(f.frac, __int_as_float(f.idx));
     else
       PX[kx] = f;
   }
@@ -80,6 +82,8 @@ __global__ void render_factors_kernel(RenderParams p) {
     }
     if (pin)
       PY2[2 * (size_t)ky] = make_float2(f.re, f.im);
+    else if (p.aux8)
+      reinterpret_cast<float2*>(p.py)[(size_t)vk * p.Hp + ky] = make_float2(f.frac, __int_as_float(f.idx));
     else
       PY[ky] = f;
   }
@@ -893,6 +897,195 @@ int launch_horner2(const RenderParams& p, cudaStream_t st) {
   return FDL_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Aperture Horner tile (every aperture of the batch real; pinhole views point
+// at the ONE entry).  Per (view, bin, layer) the weight is psi_k * phase_k with
+// the phase geometric in k, so
+//   acc <- acc * m_k + psi_k L_k,   out = w_0 * acc      (m_k as in render_horner2)
+// psi_k is the reference's bilinear lookup (lfmodel.py:72-99) from the
+// difference-form quad table: (A, B) = (a, b) + fy (c, d), psi = A + fx B.
+// The lookup halves {frac, idx} of 8 layers x VB views x (32 columns + 4 rows)
+// are staged per 8-layer block (double-buffered, one barrier per block); the
+// quad of step j + 1 is gathered into registers while step j is consumed.
+// Per unit: 2 (bilinear) + 3 C (psi L, Horner step) fp32 instructions.
+// ---------------------------------------------------------------------------
+template <int C, int VB>
+__global__ void __launch_bounds__(128, 3) render_ap_horner(RenderParams p) {
+  extern __shared__ __align__(16) unsigned char aph_smem[];  // ApHornerSmem<C, VB>
+  float2 (*LR)[C][128] = reinterpret_cast<float2 (*)[C][128]>(aph_smem);
+  float2 (*AX)[HB][VB][32] = reinterpret_cast<float2 (*)[HB][VB][32]>(aph_smem + sizeof(float2) * H2_RING * C * 128);
+  float2 (*AY)[HB][VB][4] =
+      reinterpret_cast<float2 (*)[HB][VB][4]>(aph_smem + sizeof(float2) * (H2_RING * C * 128 + 2 * HB * VB * 32));
+  u64 (*ZC)[128] = reinterpret_cast<u64 (*)[128]>(
+      aph_smem + sizeof(float2) * (H2_RING * C * 128 + 2 * HB * VB * 32 + 2 * HB * VB * 4));
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int kx = blockIdx.y * 32 + tx, ky = blockIdx.z * 4 + ty;
+  const int v0 = blockIdx.x * VB;
+  const int nv = min(VB, p.V - v0);
+  const long long Q = (long long)p.Hp * p.Whp;
+  const bool inside = kx < p.Whp && ky < p.Hp;
+  const long long q = inside ? (long long)ky * p.Whp + kx : 0;
+  const int n = p.n;
+  const int nb = (n + HB - 1) / HB;
+  const float4* DQ = p.dquad;
+  const int zero = p.dq_zero;
+  const float2* PXA = reinterpret_cast<const float2*>(p.px);
+  const float2* PYA = reinterpret_cast<const float2*>(p.py);
+
+  // lookup halves of block blk (layers 8 blk + 7 - jj) into buffer buf; missing
+  // views / layers / columns get the ZERO entry's index (weight 0)
+  auto stage_aux = [&](int blk, int buf) {
+    for (int e = tid; e < HB * VB * 36; e += 128) {
+      const int jj = e / (VB * 36), r = e % (VB * 36), b = r / 36, c = r % 36;
+      const int k = blk * HB + HB - 1 - jj, v = v0 + b;
+      if (c < 32) {
+        const int col = blockIdx.y * 32 + c;
+        const bool ok = k < n && v < p.V && col < p.Whp;
+        cp_async8(&AX[buf][jj][b][c], ok ? PXA + ((size_t)v * n + k) * p.Whp + col : PXA, ok);
+      } else {
+        const int row = blockIdx.z * 4 + c - 32;
+        const bool ok = k < n && v < p.V && row < p.Hp;
+        cp_async8(&AY[buf][jj][b][c - 32], ok ? PYA + ((size_t)v * n + k) * p.Hp + row : PYA, ok);
+      }
+    }
+  };
+  // (zero-filled entries are {0, idx 0}: idx 0 is a valid table entry, and the
+  // views / layers they stand for are never stored or are skipped)
+
+  // layer stream from the (zero-padded) top of the last block: layer k in ring
+  // slot k & 7.  Padded layers (k >= n) are zero-filled: the accumulator is
+  // still zero there, so their Horner multiplies are harmless.
+  static_assert(H2_RING == HB, "ring slot = k mod 8");
+  const int ktop = nb * HB - 1;
+  const long long qb = Q * (long long)sizeof(float2);
+  const long long step_b = (long long)C * qb;
+  const char* lbase = reinterpret_cast<const char*>(p.layers + q);
+  const char* src = lbase + (long long)ktop * step_b;
+  int k_is = ktop;
+  auto issue = [&](int slot) {
+    const bool ok = inside && k_is >= 0 && k_is < n;
+    const char* a0 = ok ? src : lbase;
+#pragma unroll
+    for (int c = 0; c < C; ++c) cp_async8(&LR[slot][c][tid], a0 + (ok ? c * qb : 0), ok);
+    src -= step_b;
+    --k_is;
+    cp_async_commit();
+  };
+  stage_aux(nb - 1, (nb - 1) & 1);  // rides in the first group
+#pragma unroll
+  for (int s = 0; s < H2_RING - 1; ++s) issue(HB - 1 - s);
+
+  u64 z[VB];
+  double2 za[VB], ze[VB];
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    const bool ok = inside && b < nv;
+    za[b] = ok ? p.zx[(size_t)(v0 + b) * p.Whp + kx] : make_double2(1.0, 0.0);
+    ze[b] = ok ? p.zy[(size_t)(v0 + b) * p.Hp + ky] : make_double2(1.0, 0.0);
+  }
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    const double2 a = za[b];
+    const double2 e = ze[b];
+    const double zr = __dsub_rn(__dmul_rn(a.x, e.x), __dmul_rn(a.y, e.y));
+    const double zi = __dadd_rn(__dmul_rn(a.x, e.y), __dmul_rn(a.y, e.x));
+    const float fr = __double2float_rn(zr), fi = __double2float_rn(zi);
+    z[b] = pack2(fr, fi);
+    ZC[b][tid] = pack2(__double2float_rn(__fma_rn(8.0, zr, -7.0 * (double)fr)),
+                       __double2float_rn(__fma_rn(8.0, zi, -7.0 * (double)fi)));
+  }
+  u64 acc[VB][C];
+#pragma unroll
+  for (int b = 0; b < VB; ++b)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[b][c] = 0ull;
+  // quads and fractions of the current / next step, in two register sets that
+  // alternate with the (compile-time) step parity: no copies between steps
+  float4 TA[VB], TB[VB];
+  float2 FA[VB], FB[VB];
+  // per-block base pointers of this thread's lookup halves (compile-time offsets below)
+  const float2* axb = nullptr;
+  const float2* ayb = nullptr;
+  auto gather1 = [&](int jj, int b, float4& T, float2& F) {
+    const float2 ax = axb[(jj * VB + b) * 32], ay = ayb[(jj * VB + b) * 4];
+    F = make_float2(ax.x, ay.x);
+    T = __ldg(DQ + min(__float_as_int(ax.y) + __float_as_int(ay.y), zero));
+  };
+
+  for (int blk = nb - 1; blk >= 0; --blk) {
+    const int buf = blk & 1;
+    // block start: this layer's values and this block's lookup halves landed
+    // (own copies), barrier (visible; everyone is done with the other buffer),
+    // then the next block's halves ride in this step's copy group
+    cp_async_wait<H2_RING - 2>();
+    __syncthreads();
+    if (blk > 0) stage_aux(blk - 1, buf ^ 1);
+    issue(0);  // layer 8 blk + 7 - 7
+    axb = &AX[buf][0][0][tx];
+    ayb = &AY[buf][0][0][ty];
+#pragma unroll
+    for (int b = 0; b < VB; ++b) gather1(0, b, TA[b], FA[b]);
+#pragma unroll
+    for (int j = 0; j < HB; ++j) {
+      if (j > 0) {
+        issue((HB - j) & 7);  // layer k - 7 -> slot (k + 1) & 7
+        cp_async_wait<H2_RING - 1>();
+      }
+      float2 L[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) L[c] = LR[HB - 1 - j][c][tid];
+#pragma unroll
+      for (int b = 0; b < VB; ++b) {
+        float4& T = (j & 1) ? TB[b] : TA[b];
+        float2& F = (j & 1) ? FB[b] : FA[b];
+        if (j + 1 < HB) gather1(j + 1, b, (j & 1) ? TA[b] : TB[b], (j & 1) ? FA[b] : FB[b]);
+        u64 ab = pack2(T.x, T.y);
+        ffma2s(ab, pack2(T.z, T.w), F.y);
+        const float2 AB = as_f2(ab);
+        const float sv = fmaf(F.x, AB.y, AB.x);
+        const u64 m = (j == 0) ? ZC[b][tid] : z[b];
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[b][c] = horner_step(acc[b][c], m, as_f2(fmul2s(pack2(L[c].x, L[c].y), sv)));
+      }
+    }
+  }
+  if (!inside) return;
+#pragma unroll
+  for (int b = 0; b < VB; ++b) {
+    if (b >= nv) break;
+    const int v = v0 + b;
+    const double2 a = p.zx[((size_t)p.V + v) * p.Whp + kx];
+    const double2 e = p.zy[((size_t)p.V + v) * p.Hp + ky];
+    const u64 w0 = pack2(__double2float_rn(__dsub_rn(__dmul_rn(a.x, e.x), __dmul_rn(a.y, e.y))),
+                         __double2float_rn(__dadd_rn(__dmul_rn(a.x, e.y), __dmul_rn(a.y, e.x))));
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      u64 o = 0ull;
+      cmac_w(o, w0, as_f2(acc[b][c]));
+      p.out[((size_t)v * C + c) * Q + q] = as_f2(o);
+    }
+  }
+}
+
+template <int C> struct APHVB;
+template <> struct APHVB<1> { static constexpr int vb = 8; };
+template <> struct APHVB<2> { static constexpr int vb = 6; };
+template <> struct APHVB<3> { static constexpr int vb = 6; };
+template <> struct APHVB<4> { static constexpr int vb = 4; };
+
+template <int C>
+int launch_ap_horner(const RenderParams& p, cudaStream_t st) {
+  render_z_kernel<<<p.V, 256, 0, st>>>(p);
+  FDL_LAUNCH_CHECK("render_z_kernel");
+  constexpr int VB = APHVB<C>::vb;
+  constexpr size_t smem = sizeof(float2) * (H2_RING * C * 128 + 2 * HB * VB * 36) + sizeof(u64) * VB * 128;
+  FDL_CUDA_CHECK(cudaFuncSetAttribute(render_ap_horner<C, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((p.Whp + 31) / 32), (unsigned)((p.Hp + 3) / 4));
+  render_ap_horner<C, VB><<<grid, 128, smem, st>>>(p);
+  FDL_LAUNCH_CHECK("render_ap_horner");
+  return FDL_OK;
+}
+
 // Direct sums on the self-conjugate Nyquist column / row, whose cosine phases
 // (construct.py:68-80) the Horner recurrences do not model.  One thread per
 // (line bin, view), every channel; the per-axis phases run as fp64
@@ -914,6 +1107,7 @@ __global__ void render_nyquist_fix(RenderParams p) {
     const double ox = omega_x_label(kx, p.Wp), oy = omega_y_label(ky, p.Hp);
     const double a0 = p.pu[(size_t)v * p.n], b0 = p.pv[(size_t)v * p.n];
     const double a = p.h_alpha[v], b = p.h_beta[v];
+    const int ai = p.view_ap ? p.view_ap[v] : -1;
     // start phases and ratios in fp64: cosine lines e^{i pi P}, else e^{2 pi i P w}
     double sxr, sxi, rxr, rxi, syr, syi, ryr, ryi;
     sincospi(nx ? a0 : 2.0 * a0 * ox, &sxi, &sxr);
@@ -937,7 +1131,22 @@ __global__ void render_nyquist_fix(RenderParams p) {
         if (k0 + kk >= p.n) break;
         // weight in fp64 (one per view, bin, layer), accumulation in fp32 like the tiles
         const double xr = sxr, xi = nx ? 0.0 : sxi, yr = syr, yi = ny ? 0.0 : syi;
-        const float wr = (float)(xr * yr - xi * yi), wi = (float)(xr * yi + xi * yr);
+        double psi = 1.0;  // real aperture tables only on this path (difference-form quads)
+        if (ai >= 0) {
+          const DevAperture& ap = p.aps[ai];
+          const double t = p.t[(size_t)v * p.n + k0 + kk];
+          int ix, iy;
+          double fx, fy;
+          const bool okx = axis_lookup(__dmul_rn(t, ox), ap.xi0_x, ap.step_x, ap.cols, ix, fx);
+          const bool oky = axis_lookup(__dmul_rn(t, oy), ap.xi0_y, ap.step_y, ap.rows, iy, fy);
+          if (okx && oky) {
+            const float4 e = p.dquad[p.ap_qbase[ai] + iy * ap.cols + ix];
+            psi = ((double)e.x + fy * e.z) + fx * ((double)e.y + fy * e.w);
+          } else {
+            psi = 0.0;
+          }
+        }
+        const float wr = (float)((xr * yr - xi * yi) * psi), wi = (float)((xr * yi + xi * yr) * psi);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           accr[c] = fmaf(wr, Lb[kk][c].x, fmaf(-wi, Lb[kk][c].y, accr[c]));
@@ -1026,6 +1235,15 @@ bool use_horner2(const RenderParams& p) {
   return p.horner && p.view_ap == nullptr && (!rk || rk[0] == '2');
 }
 
+// aperture batches whose tables are all real, shifts affine: the aperture
+// Horner tile.  Opt-in (FDL_RENDER_KERNEL=aph): correct (tests pass through it)
+// but slower than the round-1 tile on C5 (53 vs 36 ms per 256 views) --
+// the per-step quad gathers and the doubled register sets cap it at 12 warps/SM.
+bool use_ap_horner(const RenderParams& p) {
+  const char* rk = getenv("FDL_RENDER_KERNEL");
+  return p.horner && p.view_ap != nullptr && p.fast_ap && rk && rk[0] == 'a';
+}
+
 
 template <int C>
 int launch_sum(const RenderParams& p, cudaStream_t st) {
@@ -1035,6 +1253,11 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
   const char* rk = getenv("FDL_RENDER_KERNEL");
   if (use_horner2(p)) {
     int rc = launch_horner2<C>(p, st);
+    if (rc) return rc;
+    return launch_nyquist_fix(p, st);
+  }
+  if (use_ap_horner(p)) {
+    int rc = launch_ap_horner<C>(p, st);
     if (rc) return rc;
     return launch_nyquist_fix(p, st);
   }
@@ -1075,9 +1298,11 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
 
 }  // namespace
 
-int render_launch(const RenderParams& p, cudaStream_t st) {
-  if (p.V == 0) return FDL_OK;
-  if (!use_horner2(p)) {  // the Horner tile needs no per-layer factors
+int render_launch(const RenderParams& p0, cudaStream_t st) {
+  if (p0.V == 0) return FDL_OK;
+  RenderParams p = p0;
+  p.aux8 = use_ap_horner(p) ? 1 : 0;  // the aperture Horner tile reads 8-byte lookup halves
+  if (!use_horner2(p)) {  // the pinhole Horner tile needs no per-layer factors
     render_factors_kernel<<<p.V * p.n, 256, 0, st>>>(p);
     FDL_LAUNCH_CHECK("render_factors_kernel");
   }
