@@ -135,6 +135,22 @@ def test_render_c5_small_matches_reference(fdl):
         assert p >= PSNR_MIN, (i, p)
 
 
+@pytest.mark.parametrize("tile", ["legacy", "fast", "aph"])
+def test_render_c5_small_every_tile(fdl, monkeypatch, tile):
+    """The aperture render tiles behind FDL_RENDER_KERNEL (round-1 tile, direct
+    fast tile, aperture Horner tile) against the reference's renders."""
+    monkeypatch.setenv("FDL_RENDER_KERNEL", tile)
+    g = load_golden("render_c5_small")
+    n, C, hp, whp = g["layers"].shape
+    model = fdl.FdlModel(disparities=g["d"], layers=g["layers"], grid=fdl.FrequencyGrid(40, hp), width=40,
+                         height=hp)
+    ap = golden_spec(fdl, g)
+    reqs = [fdl.RenderRequest(u=g["u"][i], v=g["v"][i], s=g["s"][i], f=g["f"][i], aperture=ap)
+            for i in range(len(g["u"]))]
+    for i, img in enumerate(fdl.render_many(model, reqs)):
+        assert psnr(img, g["renders"][i]) >= PSNR_MIN, (tile, i)
+
+
 def test_render_many_matches_single(fdl):
     g = load_golden("render_c5_small")
     n, C, hp, whp = g["layers"].shape
