@@ -109,7 +109,8 @@ struct SolvePlan {
   Blob blob;
   SolveParams p{};
   size_t o_rows, o_pu, o_pv, o_d, o_d4, o_vap, o_s, o_sc, o_aps, o_cnt;
-  size_t o_uidx = 0, o_vidx = 0, o_uval = 0, o_vval = 0;
+  size_t o_uidx = 0, o_vidx = 0, o_uval = 0, o_vval = 0, o_pairs = 0;
+  bool has_pairs = false;
   size_t extra = 0;  // device-only scratch after the uploaded block (not copied)
   size_t ws_bytes() const { return blob.size() + align256(extra); }
   bool has_axes = false;
@@ -199,6 +200,9 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
     mode = MODE_REALA;
   } else if (D->force_path == 3) {
     mode = MODE_COMPLEX;
+  } else if (D->force_path == 5) {
+    if (!ok1) return fail(FDL_ERR_INVALID, "toeplitz-real path needs pinhole views and symmetric shifts");
+    mode = MODE_SYMREAL;  // without the mirror-pair split
   } else {
     mode = ok1 ? MODE_SYMREAL : (ok2 ? MODE_REALA : MODE_COMPLEX);
   }
@@ -206,6 +210,7 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
 
   SolveParams& p = P.p;
   p.m = m;
+  p.mrow = m;
   p.n = n;
   p.C = C;
   p.Hp = D->Hp;
@@ -325,6 +330,46 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
     p.fast_nu = (int)uv.size();
     p.fast_nv = (int)vv.size();
     P.has_axes = true;
+    // mirror pairs (k1_solve.cuh): every view paired with its (-u, -v) twin or at the origin
+    p.mrow = m;
+    const char* pe = getenv("FDL_K1_PAIR");
+    if (mode == MODE_SYMREAL && D->force_path != 5 && !(pe && pe[0] == '0')) {
+      std::vector<int> partner(m, -2);
+      bool all = true;
+      for (int j = 0; j < m && all; ++j) {
+        if (partner[j] != -2) continue;
+        if (D->u[j] == 0.0 && D->v[j] == 0.0) {
+          partner[j] = -1;
+          continue;
+        }
+        int f = -1;
+        for (int j2 = j + 1; j2 < m; ++j2)
+          if (partner[j2] == -2 && D->u[j2] == -D->u[j] && D->v[j2] == -D->v[j]) {
+            f = j2;
+            break;
+          }
+        if (f < 0) all = false;
+        else {
+          partner[j] = f;
+          partner[f] = j;
+        }
+      }
+      if (all) {
+        std::vector<int> rp;
+        for (int j = 0; j < m; ++j) {
+          if (partner[j] == -1) {
+            rp.push_back(j);
+            rp.push_back(-1);
+          } else if (partner[j] > j) {
+            rp.push_back(j);
+            rp.push_back(partner[j]);
+          }
+        }
+        p.mrow = (int)rp.size() / 2;
+        P.o_pairs = B.add(rp.data(), sizeof(int) * rp.size());
+        P.has_pairs = true;
+      }
+    }
     // per-axis phase tables of the fast path: (Whp nu + nrows nv) (n/2 + 1) complex doubles
     const size_t hw = (size_t)(n / 2 + (n & 1));
     P.extra = 16 * hw * ((size_t)p.Whp * p.fast_nu + (size_t)D->nrows * p.fast_nv);
@@ -349,7 +394,9 @@ void bind_solve(SolvePlan& P, const fdl_solve_desc* D, void* ws) {
     p.fast_u_val = at<double>(ws, P.o_uval);
     p.fast_v_val = at<double>(ws, P.o_vval);
     p.fast_tables = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + P.blob.size());
+    p.row_pairs = P.has_pairs ? at<int2>(ws, P.o_pairs) : nullptr;
   } else {
+    p.row_pairs = nullptr;
     p.fast_tables = nullptr;
     p.fast_u_idx = p.fast_v_idx = nullptr;
     p.fast_u_val = p.fast_v_val = nullptr;

@@ -96,6 +96,9 @@ struct FastParams {
 };
 
 __host__ __device__ constexpr int blk(int I, int J) { return I * (I + 1) / 2 + J; }
+// mode 1 block groups: 0 = cos half (+ the middle column of odd n), 1 = sin half.
+// With mirror pairs (PAIR) blocks of different groups are exactly zero.
+__host__ __device__ constexpr int grp(int I, int NBc) { return (I >= NBc && I < 2 * NBc) ? 1 : 0; }
 
 // mode 2: per-(view, layer) half of the aperture lookup, shared by a CTA's row of bins
 struct YEntry {
@@ -129,9 +132,11 @@ __global__ void k1_axis_tables_kernel(SolveParams p, FastParams f) {
   }
 }
 
-template <int NB, int MODE, int ODD>
+template <int NB, int MODE, int ODD, int PAIR>
 __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1))) k1_fast_kernel(SolveParams p, FastParams f) {
   constexpr int NBc = (NB - ODD) / 2;  // blocks of the cos half (= of the sin half), mode 1
+  // blocks I, J interact (PAIR: only within a group)
+  auto linked = [](int I, int J) { return !PAIR || grp(I, NBc) == grp(J, NBc); };
   constexpr int NBLK = NB * (NB + 1) / 2;
   constexpr int NP = NB * 8;
   extern __shared__ double smem[];
@@ -145,9 +150,12 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
   double* PY = smem;
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
-  const int m4 = (p.m + 3) & ~3;
-  const int ro_words = (MODE == MODE_SYMREAL) ? m4 : 3 * p.m * p.n;  // mode 2: YEntry per (view, layer)
-  int2* ROWOFF = reinterpret_cast<int2*>(PY + py_words);
+  // mode 1 equation rows: one per view, or one per mirror pair (p.mrow)
+  const int mrow = (MODE == MODE_SYMREAL) ? p.mrow : p.m;
+  const int m4 = (mrow + 3) & ~3;
+  const int ro_words = (MODE == MODE_SYMREAL) ? 2 * m4 : 3 * p.m * p.n;  // mode 2: YEntry per (view, layer)
+  // mode 1: per row (u-table offset, v-table offset, BS offset of j, of j' or -1)
+  int4* ROW4 = reinterpret_cast<int4*>(PY + py_words);
   YEntry* YT = reinterpret_cast<YEntry*>(PY + py_words);
   const int bs_words = (p.m * p.C + 1) & ~1;  // staged spectra, one float2 per (view, channel); keeps 16-B alignment
   const int per_warp = px_words + 8 * LD + 8 * LD + NB * 8 * LD + NP * LD + bs_words;
@@ -165,8 +173,14 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
       const int rr = e / f.hw;
       reinterpret_cast<double2*>(PY)[rr * f.hwp + (e - rr * f.hw)] = src[e];
     }
-    for (int e = threadIdx.x; e < m4; e += blockDim.x)
-      ROWOFF[e] = e < p.m ? make_int2(f.u_idx[e] * f.hwp, f.v_idx[e] * f.hwp) : make_int2(0, 0);
+    for (int e = threadIdx.x; e < m4; e += blockDim.x) {
+      int4 ro = make_int4(0, 0, 0, -1);
+      if (e < mrow) {
+        const int2 jj = PAIR ? p.row_pairs[e] : make_int2(e, -1);
+        ro = make_int4(f.u_idx[jj.x] * f.hwp, f.v_idx[jj.x] * f.hwp, jj.x * p.C, jj.y >= 0 ? jj.y * p.C : -1);
+      }
+      ROW4[e] = ro;
+    }
   } else {
     // mode 2: the y half of every bilinear lookup depends only on (view, layer, row):
     // t_jk = scale_j (s_j - d_k), (iy, fy) of t_jk wy -- shared by the CTA's bins
@@ -265,19 +279,38 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
   // one k-step: 4 rows (views) r0..r0+3, lane row j = r0 + t
   auto kstep = [&](int r0, bool tail) {
     const int j = r0 + t;
-    const bool valid = !tail || j < p.m;
-    const float2 bcur = BS[(valid ? j : 0) * p.C + bc];
+    const bool valid = !tail || j < mrow;
     double mf[NB];
 #pragma unroll
     for (int I = 0; I < NB; ++I) mf[I] = 0.0;
-    double bf = bcol ? ((q & 1) ? (double)bcur.y : (double)bcur.x) : 0.0;
+    double bf = 0.0;   // B fragment (RHS columns); PAIR: of the cos group (b_j + b_j')
+    double bfm = 0.0;  // PAIR: B fragment of the sin group (b_j - b_j')
+    bool paired = false;
     if (MODE == MODE_SYMREAL) {
-      const int2 ro = ROWOFF[j];
+      const int4 ro = ROW4[j];
+      const float2 b1 = BS[ro.z + bc];
+      const double v1 = bcol ? ((q & 1) ? (double)b1.y : (double)b1.x) : 0.0;
+      if (PAIR) {
+        paired = ro.w >= 0;
+        const float2 b2 = BS[paired ? ro.w + bc : bc];
+        const double v2 = (bcol && paired) ? ((q & 1) ? (double)b2.y : (double)b2.x) : 0.0;
+        bf = v1 + v2;
+        bfm = v1 - v2;
+      } else {
+        bf = v1;
+      }
       const double2* pxr = PX2 + ro.x;
       const double2* pyr = PY2 + ro.y;
       if (th && q >= 6) {
         const double2 x0 = pxr[0], y0 = pyr[0];
-        bf = (q == 6) ? fma(x0.x, y0.x, -x0.y * y0.y) : fma(x0.x, y0.y, x0.y * y0.x);
+        const double re = fma(x0.x, y0.x, -x0.y * y0.y), im = fma(x0.x, y0.y, x0.y * y0.x);
+        if (PAIR) {
+          // the partner's A_j'0 = conj(A_j0): column 6 (Re) sums, column 7 (Im) cancels
+          bf = (q == 6) ? (paired ? 2.0 * re : re) : (paired ? 0.0 : im);
+          bfm = (q == 6) ? (paired ? 0.0 : re) : (paired ? 2.0 * im : im);
+        } else {
+          bf = (q == 6) ? re : im;
+        }
       }
 #pragma unroll
       for (int I = 0; I < NBc; ++I) {
@@ -295,10 +328,11 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
       if (tail && !valid) {
 #pragma unroll
         for (int I = 0; I < NB; ++I) mf[I] = 0.0;
-        bf = 0.0;
+        bf = bfm = 0.0;
       }
     } else {  // MODE_REALA: A_jk = psi_j(t_jk wx, t_jk wy) (all shifts are zero)
-      if (!valid) bf = 0.0;
+      const float2 bcur = BS[(valid ? j : 0) * p.C + bc];
+      bf = (bcol && valid) ? ((q & 1) ? (double)bcur.y : (double)bcur.x) : 0.0;
 #pragma unroll
       for (int I = 0; I < NB; ++I) {
         const int k = I * 8 + q;
@@ -340,18 +374,21 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
       }
     }
 #pragma unroll
-    for (int I = 0; I < NB; ++I) dmma(r[I], mf[I], bf);
+    for (int I = 0; I < NB; ++I) dmma(r[I], mf[I], (PAIR && grp(I, NBc)) ? bfm : bf);
     if (!th) {
+      // PAIR: a pair row stands for two views with equal c c^T and s s^T terms
+      const double w = paired ? 2.0 : 1.0;
 #pragma unroll
       for (int I = 0; I < NB; ++I)
 #pragma unroll
-        for (int J = 0; J <= I; ++J) dmma(g[blk(I, J)], mf[I], mf[J]);
+        for (int J = 0; J <= I; ++J)
+          if (linked(I, J)) dmma(g[blk(I, J)], mf[I], PAIR ? w * mf[J] : mf[J]);
     }
   };
-  const int mfull = p.m & ~3;
+  const int mfull = mrow & ~3;
 #pragma unroll kKUnroll
   for (int r0 = 0; r0 < mfull; r0 += 4) kstep(r0, false);
-  if (mfull < p.m) kstep(mfull, true);
+  if (mfull < mrow) kstep(mfull, true);
   __syncwarp();  // every lane is done with BS / PX of this bin
   if (has_next) stage_bin(kx_next);
 
@@ -397,6 +434,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
       for (int J = 0; J <= I; ++J)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
+          if (!linked(I, J)) continue;
           // quadrant (cos / sin / middle) of block row I and block column J is compile-time
           const bool rc = I < NBc, rs = I >= NBc && I < 2 * NBc;
           const bool cc_ = J < NBc, cs = J >= NBc && J < 2 * NBc;
@@ -452,95 +490,119 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
   }
 
   // ---------------------------------------------------------------- 3. Cholesky + forward
+  // Steps of one diagonal block, or (PAIR) of two -- cos block s and sin block
+  // NBc + s, factored side by side by lanes 0..7 and 8..15 -- then the middle
+  // block of odd n.
   bool ok = true;
+  constexpr int NSTEP = PAIR ? NBc + ODD : NB;
 #pragma unroll
-  for (int K = 0; K < NB; ++K) {
-    // (a) factor the diagonal block with lanes 0..7 (lane = row) and invert it;
-    //     column values are broadcast through shared memory, pivots by rsqrt.
-    store_c(S, g[blk(K, K)], lane);
+  for (int st = 0; st < NSTEP; ++st) {
+    const int Ka = PAIR ? (st < NBc ? st : NB - 1) : st;
+    const int Kb = PAIR && st < NBc ? NBc + st : -1;
+    // (a) factor the diagonal block(s) with 8 lanes each (lane = row) and invert;
+    //     column values are broadcast by shuffles, pivots by rsqrt.
+    store_c(S, g[blk(Ka, Ka)], lane);
+    if (Kb >= 0) store_c(T, g[blk(Kb, Kb)], lane);
     __syncwarp();
     bool lok = true;
-    if (lane < 8) {
+    if (lane < 16) {
+      const int hi = lane >> 3, row = lane & 7;
+      const bool own = hi == 0 || Kb >= 0;  // lanes 8..15 of a one-block step repeat lanes 0..7
+      double* Sx = (hi && Kb >= 0) ? T : S;
       double a[8], dinv[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) a[c] = S[lane * LD + c];
+      for (int c = 0; c < 8; ++c) a[c] = Sx[row * LD + c];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const double akk = __shfl_sync(0xffu, a[k], k);
+        const double akk = __shfl_sync(0xffffu, a[k], (lane & 8) | k);
         const bool good = (akk > 0.0) && isfinite(akk);
         lok = lok && good;
         const double inv = rsqrt_fast(good ? akk : 1.0);
         dinv[k] = inv;
-        a[k] = (lane == k) ? (good ? akk : 1.0) * inv : a[k] * inv;  // rows < k: unused upper part
+        a[k] = (row == k) ? (good ? akk : 1.0) * inv : a[k] * inv;  // rows < k: unused upper part
 #pragma unroll
-        for (int c = k + 1; c < 8; ++c) a[c] = fma(-a[k], __shfl_sync(0xffu, a[k], c), a[c]);  // upper: harmless
+        for (int c = k + 1; c < 8; ++c) a[c] = fma(-a[k], __shfl_sync(0xffffu, a[k], (lane & 8) | c), a[c]);  // upper: harmless
       }
+      __syncwarp(0xffffu);
+      if (own) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) S[lane * LD + c] = a[c];  // upper triangle ignored below
-      __syncwarp(0xffu);
-      // column `lane` of W = L^-1: w_rr = (delta_rc - sum_{k<rr} L_rk w_k) / L_rr  (zero above c)
-      const int c = lane;
+        for (int c = 0; c < 8; ++c) Sx[row * LD + c] = a[c];  // upper triangle ignored below
+      }
+      __syncwarp(0xffffu);
+      // column `row` of W = L^-1: w_rr = (delta_rc - sum_{k<rr} L_rk w_k) / L_rr  (zero above c)
+      const int c = row;
       double w[8];
 #pragma unroll
       for (int rr = 0; rr < 8; ++rr) {
         double acc = (rr == c) ? 1.0 : 0.0;
 #pragma unroll
-        for (int k = 0; k < rr; ++k) acc = fma(-S[rr * LD + k], w[k], acc);
+        for (int k = 0; k < rr; ++k) acc = fma(-Sx[rr * LD + k], w[k], acc);
         w[rr] = acc * dinv[rr];
       }
+      if (own) {
+        double* Wd = Wst + (hi ? Kb : Ka) * 8 * LD;
 #pragma unroll
-      for (int rr = 0; rr < 8; ++rr) Wst[K * 8 * LD + rr * LD + c] = w[rr];
+        for (int rr = 0; rr < 8; ++rr) Wd[rr * LD + c] = w[rr];
+      }
     }
     ok = ok && __all_sync(FULL, lok);
     __syncwarp();
-    const double* Wk = Wst + K * 8 * LD;
-    // A-fragment of W (= B-fragment of W^T): W[q][t], W[q][4+t]
-    const double wa0 = Wk[q * LD + t], wa1 = Wk[q * LD + 4 + t];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int K = side ? Kb : Ka;
+      if (K < 0) continue;
+      const double* Wk = Wst + K * 8 * LD;
+      // A-fragment of W (= B-fragment of W^T): W[q][t], W[q][4+t]
+      const double wa0 = Wk[q * LD + t], wa1 = Wk[q * LD + 4 + t];
 
-    // (b) panel L_IK = G_IK W^T, kept in place (accumulator layout) and as A-fragments
-    double lf[NB][2];
-#pragma unroll
-    for (int I = K + 1; I < NB; ++I) {
-      double a0, a1;
-      c_to_a(g[blk(I, K)], a0, a1, lane);
-      double d[2] = {0.0, 0.0};
-      dmma(d, a0, wa0);
-      dmma(d, a1, wa1);
-      g[blk(I, K)][0] = d[0];
-      g[blk(I, K)][1] = d[1];
-      c_to_a(d, lf[I][0], lf[I][1], lane);
-    }
-    // (c) trailing update
-#pragma unroll
-    for (int I = K + 1; I < NB; ++I)
-#pragma unroll
-      for (int J = K + 1; J <= I; ++J) {
-        dmma(g[blk(I, J)], -lf[I][0], lf[J][0]);
-        dmma(g[blk(I, J)], -lf[I][1], lf[J][1]);
-      }
-    // (d) forward substitution: y_K = W r_K; r_I -= L_IK y_K
-    store_c(T, r[K], lane);
-    __syncwarp();
-    {
-      const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
-      double y[2] = {0.0, 0.0};
-      dmma(y, wa0, b0);
-      dmma(y, wa1, b1);
-      r[K][0] = y[0];
-      r[K][1] = y[1];
-    }
-    __syncwarp();
-    store_c(T, r[K], lane);
-    __syncwarp();
-    {
-      const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
+      // (b) panel L_IK = G_IK W^T, kept in place (accumulator layout) and as A-fragments
+      double lf[NB][2];
 #pragma unroll
       for (int I = K + 1; I < NB; ++I) {
-        dmma(r[I], -lf[I][0], b0);
-        dmma(r[I], -lf[I][1], b1);
+        if (!linked(I, K)) continue;
+        double a0, a1;
+        c_to_a(g[blk(I, K)], a0, a1, lane);
+        double d[2] = {0.0, 0.0};
+        dmma(d, a0, wa0);
+        dmma(d, a1, wa1);
+        g[blk(I, K)][0] = d[0];
+        g[blk(I, K)][1] = d[1];
+        c_to_a(d, lf[I][0], lf[I][1], lane);
       }
+      // (c) trailing update
+#pragma unroll
+      for (int I = K + 1; I < NB; ++I)
+#pragma unroll
+        for (int J = K + 1; J <= I; ++J) {
+          if (!linked(I, K) || !linked(J, K)) continue;
+          dmma(g[blk(I, J)], -lf[I][0], lf[J][0]);
+          dmma(g[blk(I, J)], -lf[I][1], lf[J][1]);
+        }
+      // (d) forward substitution: y_K = W r_K; r_I -= L_IK y_K
+      store_c(T, r[K], lane);
+      __syncwarp();
+      {
+        const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
+        double y[2] = {0.0, 0.0};
+        dmma(y, wa0, b0);
+        dmma(y, wa1, b1);
+        r[K][0] = y[0];
+        r[K][1] = y[1];
+      }
+      __syncwarp();
+      store_c(T, r[K], lane);
+      __syncwarp();
+      {
+        const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
+#pragma unroll
+        for (int I = K + 1; I < NB; ++I) {
+          if (!linked(I, K)) continue;
+          dmma(r[I], -lf[I][0], b0);
+          dmma(r[I], -lf[I][1], b1);
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
 
   // ---------------------------------------------------------------- 4. backward
@@ -549,6 +611,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     double z[2] = {r[K][0], r[K][1]};
 #pragma unroll
     for (int I = K + 1; I < NB; ++I) {
+      if (!linked(I, K)) continue;
       double a0, a1;
       c_to_at(g[blk(I, K)], a0, a1, lane);  // L_IK^T
       const double b0 = X[(I * 8 + t) * LD + q], b1 = X[(I * 8 + 4 + t) * LD + q];
@@ -605,15 +668,15 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
   }  // bins of this warp
 }
 
-template <int NB, int MODE, int ODD>
+template <int NB, int MODE, int ODD, int PAIR>
 int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
-  const int ro_words = (MODE == MODE_SYMREAL) ? ((p.m + 3) & ~3) : 3 * p.m * p.n;
+  const int ro_words = (MODE == MODE_SYMREAL) ? 2 * ((p.mrow + 3) & ~3) : 3 * p.m * p.n;
   const size_t smem = sizeof(double) * ((size_t)py_words + ro_words +
                                         (size_t)WARPS * (px_words + 16 * LD + NB * 8 * LD + NB * 8 * LD + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
   if (smem > 220 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
-  auto kern = k1_fast_kernel<NB, MODE, ODD>;
+  auto kern = k1_fast_kernel<NB, MODE, ODD, PAIR>;
   FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (p.reps < 1) return fail(FDL_ERR_INVALID, "K1 fast path: reps < 1");
   dim3 grid((unsigned)((p.Whp + WARPS * p.reps - 1) / (WARPS * p.reps)), (unsigned)p.nrows);
@@ -622,17 +685,17 @@ int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
   return FDL_OK;
 }
 
-template <int MODE, int ODD>
+template <int MODE, int ODD, int PAIR>
 int dispatch_nb(int NB, const SolveParams& p, const FastParams& f, cudaStream_t st) {
   switch (NB) {
-    case 1: return launch_fast<1, MODE, ODD>(p, f, st);
-    case 2: return launch_fast<2, MODE, ODD>(p, f, st);
-    case 3: return launch_fast<3, MODE, ODD>(p, f, st);
-    case 4: return launch_fast<4, MODE, ODD>(p, f, st);
-    case 5: return launch_fast<5, MODE, ODD>(p, f, st);
-    case 6: return launch_fast<6, MODE, ODD>(p, f, st);
-    case 7: return launch_fast<7, MODE, ODD>(p, f, st);
-    case 8: return launch_fast<8, MODE, ODD>(p, f, st);
+    case 1: return launch_fast<1, MODE, ODD, PAIR>(p, f, st);
+    case 2: return launch_fast<2, MODE, ODD, PAIR>(p, f, st);
+    case 3: return launch_fast<3, MODE, ODD, PAIR>(p, f, st);
+    case 4: return launch_fast<4, MODE, ODD, PAIR>(p, f, st);
+    case 5: return launch_fast<5, MODE, ODD, PAIR>(p, f, st);
+    case 6: return launch_fast<6, MODE, ODD, PAIR>(p, f, st);
+    case 7: return launch_fast<7, MODE, ODD, PAIR>(p, f, st);
+    case 8: return launch_fast<8, MODE, ODD, PAIR>(p, f, st);
     default: return fail(FDL_ERR_UNSUPPORTED, "NB");
   }
 }
@@ -722,9 +785,11 @@ int k1_fast_launch(const SolveParams& p, cudaStream_t st, bool* handled) {
     int blocks = (int)std::min<long long>((tot + 255) / 256, 148LL * 8);
     k1_axis_tables_kernel<<<blocks, 256, 0, st>>>(p, f);
     FDL_LAUNCH_CHECK("k1_axis_tables_kernel");
-    return (p.n & 1) ? dispatch_nb<MODE_SYMREAL, 1>(NB, p, f, st) : dispatch_nb<MODE_SYMREAL, 0>(NB, p, f, st);
+    if (p.row_pairs)
+      return (p.n & 1) ? dispatch_nb<MODE_SYMREAL, 1, 1>(NB, p, f, st) : dispatch_nb<MODE_SYMREAL, 0, 1>(NB, p, f, st);
+    return (p.n & 1) ? dispatch_nb<MODE_SYMREAL, 1, 0>(NB, p, f, st) : dispatch_nb<MODE_SYMREAL, 0, 0>(NB, p, f, st);
   }
-  return dispatch_nb<MODE_REALA, 0>(NB, p, f, st);
+  return dispatch_nb<MODE_REALA, 0, 0>(NB, p, f, st);
 }
 
 }  // namespace fdl

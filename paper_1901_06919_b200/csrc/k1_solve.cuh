@@ -14,6 +14,13 @@
 //      M = A U real: M[:, p] = sqrt2 Re A_p, M[:, h+p] = -sqrt2 Im A_p (p < h = n/2),
 //      M[:, 2h] = Re A_mid for odd n.  Re b and Im b are independent right-hand
 //      sides (R = 2C); N = n.  reg'_p = reg'_{h+p} = reg_p.
+//      Mirror pairs: if every view j has a partner j' with (u, v)_j' = -(u, v)_j
+//      (or sits at the origin), then A_j'k = conj(A_jk), so Re A_j' = Re A_j and
+//      Im A_j' = -Im A_j.  Summing the pair's normal-equation contributions,
+//          G = sum_j M_j^T M_j = [[2 sum' c c^T, 0], [0, 2 sum' s s^T]] (+ origin rows),
+//          M^T b = [sum' c (b_j + b_j'); -sum' s (b_j - b_j')],
+//      (sum' over one view per pair), the cos and sin halves decouple exactly:
+//      two independent systems of half the size, each built from half the rows.
 //  REALA   (mode 2): every P = 0 (all views at u = v = 0, the focal-stack
 //      input, construct.py:170-179) and real aperture tables -> A is real:
 //      M = A, R = 2C, N = n.
@@ -57,6 +64,12 @@ struct SolveParams {
   const double* fast_v_val;
   int fast_nu, fast_nv;
   double* fast_tables;       // workspace for the per-axis phase tables (fast path)
+  // SYMREAL with a mirror-symmetric view set (every view j has a partner j'
+  // with (u, v)_j' = -(u, v)_j, or sits at u = v = 0): the fast path sums the
+  // pair's equations (see the header) and solves the cos and sin halves as two
+  // independent systems.  row_pairs[r] = (j, j' or -1), r < mrow.
+  const int2* row_pairs;     // nullptr: no pairing (mrow = m)
+  int mrow;
 };
 
 // spectra / layers addressing: slab buffers or full-grid buffers (plane_rows)

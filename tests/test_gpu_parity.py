@@ -85,6 +85,37 @@ def test_construct_other_paths_agree(fdl, name, force):
     assert err <= max(LAYER_TOL, 10 * float(np.max(g["floor"])))
 
 
+@pytest.mark.parametrize("name", ["c1_full", "c2_s24", "odd_grid_n5"])
+def test_mirror_pair_split_agrees(fdl, name):
+    # the symmetric-real path splits mirror-symmetric view sets into two
+    # half-size systems (k1_solve.cuh); force_path=5 solves the unsplit system
+    g = load_golden(name)
+    split = build(fdl, g)
+    whole = build(fdl, g, force_path=5)
+    assert fdl.last_construct_stats().path == 1
+    floor = max(LAYER_TOL, 10 * float(np.max(g["floor"])))
+    e_split, e_whole = rel_l2(split.layers, g["layers"]), rel_l2(whole.layers, g["layers"])
+    print(f"{name}: split {e_split:.3e} unsplit {e_whole:.3e}")
+    assert e_split <= floor and e_whole <= floor
+
+
+def test_asymmetric_view_set_matches_oracle(fdl):
+    # a view without its mirror twin disables the pair split: the unsplit
+    # symmetric-real system must still match the oracle
+    from oracle import fdl_oracle as O
+    g = load_golden("c2_s24")
+    keep = np.ones(len(g["u"]), bool)
+    keep[np.flatnonzero((g["u"] == 1) & (g["v"] == 2))[0]] = False
+    u, v, views = g["u"][keep], g["v"][keep], g["views"][keep]
+    sh = fdl.ShiftParams.factored(u, v, g["d"])
+    model = fdl.construct_fdl(fdl.ViewSet(images=views, u=u, v=v), sh)
+    assert fdl.last_construct_stats().path == 1
+    ref = O.construct(views, np.outer(u, g["d"]), np.outer(v, g["d"]), g["d"])
+    err = rel_l2(model.layers, ref["layers"])
+    print(f"asymmetric view set: {err:.3e}")
+    assert err <= max(LAYER_TOL, 10 * float(np.max(g["floor"])))
+
+
 @pytest.mark.parametrize("name", CASES)
 def test_render_matches_reference(fdl, name):
     g = load_golden(name)
