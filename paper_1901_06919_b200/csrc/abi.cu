@@ -370,9 +370,11 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
         P.has_pairs = true;
       }
     }
-    // per-axis phase tables of the fast path: (Whp nu + nrows nv) (n/2 + 1) complex doubles
+    // per-axis phase tables of the fast path: (Whp nu + nrows nv) hwp complex doubles,
+    // hwp = the K1 shared-memory pitch of the n/2 + 1 entries (k1_dmma.cu)
     const size_t hw = (size_t)(n / 2 + (n & 1));
-    P.extra = 16 * hw * ((size_t)p.Whp * p.fast_nu + (size_t)D->nrows * p.fast_nv);
+    const size_t hwp = hw + ((2 - hw % 8) + 8) % 8;
+    P.extra = 16 * hwp * ((size_t)p.Whp * p.fast_nu + (size_t)D->nrows * p.fast_nv);
   }
   return FDL_OK;
 }

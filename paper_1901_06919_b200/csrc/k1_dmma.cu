@@ -37,6 +37,9 @@ constexpr int LD = 8;
 #define FDL_K1_KUNROLL 2
 #endif
 constexpr int kKUnroll = FDL_K1_KUNROLL;  // k-step loop unroll (A/B builds)
+#ifndef FDL_K1_PAIR3
+#define FDL_K1_PAIR3 0  // PAIR kernels with NB <= this get 3 CTAs/SM (A/B)
+#endif
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -75,10 +78,22 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   return y;
 }
 
+// accumulator fragment -> row-major 8x8 block (row stride LD): one 16-byte
+// store per lane, conflict-free (a quarter warp covers all 32 banks)
 __device__ __forceinline__ void store_c(double* S, const double (&c)[2], int lane) {
   const int q = lane >> 2, t = lane & 3;
-  S[q * LD + 2 * t] = c[0];
-  S[q * LD + 2 * t + 1] = c[1];
+  *reinterpret_cast<double2*>(S + q * LD + 2 * t) = make_double2(c[0], c[1]);
+}
+// Diagonal-block scratch: row stride LDD = 9 doubles, so the 8 rows' column c
+// fall on distinct banks (the factorisation's lane = row accesses); the
+// second block's scratch starts an odd number of doubles later, so the two
+// 8-lane groups of a paired step never share a bank either.
+constexpr int LDD = 9;
+constexpr int DSZ = 8 * LDD + 1;
+__device__ __forceinline__ void store_cd(double* D, const double (&c)[2], int lane) {
+  const int q = lane >> 2, t = lane & 3;
+  D[q * LDD + 2 * t] = c[0];
+  D[q * LDD + 2 * t + 1] = c[1];
 }
 
 struct FastParams {
@@ -91,8 +106,8 @@ struct FastParams {
   int hw;               // phase-table width: h + (n odd)
   int hwp;              // shared-memory row pitch of the tables (double2): = 2 mod 8, so the
                         // 4 views x 2 layers of a quarter-warp hit distinct banks
-  const double2* px_all;  // (Whp, nu, hw) exp(2 pi i fl(u d_p) wx), cosine on the Nyquist column
-  const double2* py_all;  // (nrows, nv, hw)
+  const double2* px_all;  // (Whp, nu, hwp) exp(2 pi i fl(u d_p) wx), cosine on the Nyquist column
+  const double2* py_all;  // (nrows, nv, hwp); the shared-memory pitch, so staging is a flat copy
 };
 
 __host__ __device__ constexpr int blk(int I, int J) { return I * (I + 1) / 2 + J; }
@@ -110,30 +125,32 @@ struct YEntry {
 // reference's `_phase_tables`, construct.py:68-80, restricted to the distinct
 // u and v values and the first half of the layers).
 __global__ void k1_axis_tables_kernel(SolveParams p, FastParams f) {
-  const long long nx = (long long)p.Whp * f.nu * f.hw;
-  const long long ny = (long long)p.nrows * f.nv * f.hw;
+  const long long nx = (long long)p.Whp * f.nu * f.hwp;
+  const long long ny = (long long)p.nrows * f.nv * f.hwp;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nx + ny;
        e += (long long)gridDim.x * blockDim.x) {
     if (e < nx) {
-      const int pp = (int)(e % f.hw);
-      const long long r = e / f.hw;
+      const int pp = (int)(e % f.hwp);
+      const long long r = e / f.hwp;
       const int iu = (int)(r % f.nu), kx = (int)(r / f.nu);
-      cd ph = axis_phase(f.u_val[iu] * p.d[pp], omega_x_label(kx, p.Wp), (p.Wp % 2 == 0) && kx == p.Wp / 2);
+      cd ph{0.0, 0.0};  // pitch padding stays zero
+      if (pp < f.hw) ph = axis_phase(f.u_val[iu] * p.d[pp], omega_x_label(kx, p.Wp), (p.Wp % 2 == 0) && kx == p.Wp / 2);
       const_cast<double2*>(f.px_all)[e] = make_double2(ph.re, ph.im);
     } else {
       const long long e2 = e - nx;
-      const int pp = (int)(e2 % f.hw);
-      const long long r = e2 / f.hw;
+      const int pp = (int)(e2 % f.hwp);
+      const long long r = e2 / f.hwp;
       const int iv = (int)(r % f.nv), i = (int)(r / f.nv);
       const int ky = p.rows[i];
-      cd ph = axis_phase(f.v_val[iv] * p.d[pp], omega_y_label(ky, p.Hp), (p.Hp % 2 == 0) && ky == p.Hp / 2);
+      cd ph{0.0, 0.0};
+      if (pp < f.hw) ph = axis_phase(f.v_val[iv] * p.d[pp], omega_y_label(ky, p.Hp), (p.Hp % 2 == 0) && ky == p.Hp / 2);
       const_cast<double2*>(f.py_all)[e2] = make_double2(ph.re, ph.im);
     }
   }
 }
 
 template <int NB, int MODE, int ODD, int PAIR>
-__global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1))) k1_fast_kernel(SolveParams p, FastParams f) {
+__global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_K1_PAIR3 ? 3 : (NB <= 6 ? 2 : 1)))) k1_fast_kernel(SolveParams p, FastParams f) {
   constexpr int NBc = (NB - ODD) / 2;  // blocks of the cos half (= of the sin half), mode 1
   // blocks I, J interact (PAIR: only within a group)
   auto linked = [](int I, int J) { return !PAIR || grp(I, NBc) == grp(J, NBc); };
@@ -146,7 +163,11 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
   const double oy = omega_y_label(ky, p.Hp);
   const bool nyq_y = (p.Hp % 2 == 0) && ky == p.Hp / 2;
 
-  // shared layout: [PY: nv*hw complex] then per warp [PX: nu*hw complex | S 64 | T 64 | Wst NB*64 | X NP*8]
+  // shared layout: [PY: nv*hwp complex | ROW4 | RG] then per warp
+  // [PX: nu*hwp complex | D 2*73 | S 64 | Wst (NB-1)*64 | X NP*8 | BS].  Lifetimes let
+  // buffers double up: T (the forward / backward 8x8 scratch) is X's first
+  // block, the W = L^-1 of the last diagonal block lives in S, and the
+  // Toeplitz build keeps t[] in X's upper half and E in its lower half.
   double* PY = smem;
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
@@ -158,21 +179,25 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
   int4* ROW4 = reinterpret_cast<int4*>(PY + py_words);
   YEntry* YT = reinterpret_cast<YEntry*>(PY + py_words);
   const int bs_words = (p.m * p.C + 1) & ~1;  // staged spectra, one float2 per (view, channel); keeps 16-B alignment
-  const int per_warp = px_words + 8 * LD + 8 * LD + NB * 8 * LD + NP * LD + bs_words;
-  double* base = smem + py_words + ro_words + warp * per_warp;
+  const int per_warp = px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + NP * LD + bs_words;
+  // per column of the real system: (d^4 of its layer(s)) for the lam reg' diagonal
+  const int rg_off = py_words + ((ro_words + 1) & ~1);  // 16-byte aligned
+  double2* RG = reinterpret_cast<double2*>(smem + rg_off);
+  double* base = smem + rg_off + 2 * NP + warp * per_warp;
   double* PX = base;
-  double* S = PX + px_words;
-  double* T = S + 8 * LD;
-  double* Wst = T + 8 * LD;
-  double* X = Wst + NB * 8 * LD;
+  double* D0 = PX + px_words;  // diagonal-block scratch (LDD layout) of block Ka ...
+  double* D1 = D0 + DSZ;       // ... and of Kb
+  double* S = D1 + DSZ;
+  double* Wst = S + 8 * LD;
+  double* X = Wst + (NB - 1) * 8 * LD;
+  double* T = X;
+  // W = L_KK^-1 of diagonal block K
+  auto Wblk = [&](int K) { return K == NB - 1 ? S : Wst + K * 8 * LD; };
   float2* BS = reinterpret_cast<float2*>(X + NP * LD);
 
   if (MODE == MODE_SYMREAL) {
-    const double2* src = f.py_all + (size_t)i * f.nv * f.hw;
-    for (int e = threadIdx.x; e < f.nv * f.hw; e += blockDim.x) {
-      const int rr = e / f.hw;
-      reinterpret_cast<double2*>(PY)[rr * f.hwp + (e - rr * f.hw)] = src[e];
-    }
+    const double2* src = f.py_all + (size_t)i * f.nv * f.hwp;
+    for (int e = threadIdx.x; e < f.nv * f.hwp; e += blockDim.x) reinterpret_cast<double2*>(PY)[e] = src[e];
     for (int e = threadIdx.x; e < m4; e += blockDim.x) {
       int4 ro = make_int4(0, 0, 0, -1);
       if (e < mrow) {
@@ -204,6 +229,20 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
       YT[e] = ye;
     }
   }
+  for (int col = threadIdx.x; col < NP; col += blockDim.x) {
+    // (d4_p, d4_{n-1-p}) for a symmetric pair, (d4_k, -1) for one layer, (-1, -1) for padding
+    double2 ab = make_double2(-1.0, -1.0);
+    if (MODE == MODE_SYMREAL) {
+      const int I = col >> 3;
+      const bool cpart = I < NBc, spart = I >= NBc && I < 2 * NBc;
+      const int pp = cpart ? col : (spart ? col - NBc * 8 : p.h);
+      if ((cpart || spart) && pp < p.h) ab = make_double2(p.d4[pp], p.d4[p.n - 1 - pp]);
+      else if (!cpart && !spart && ODD && col == 2 * NBc * 8) ab = make_double2(p.d4[p.h], -1.0);
+    } else if (col < p.n) {
+      ab = make_double2(p.d4[col], -1.0);
+    }
+    RG[col] = ab;
+  }
   __syncthreads();
   // no block barriers below: each warp solves p.reps bins of this row,
   // columns (blockIdx.x * reps + rep) * WARPS + warp
@@ -229,11 +268,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     const float2* src = p.spectra + sp_boff(p, i, kxs);
     for (int e = lane; e < p.m * p.C; e += 32) cpa8(&BS[e], src + (size_t)e * plane_, true);
     if (MODE == MODE_SYMREAL) {
-      const double2* srcx = f.px_all + (size_t)kxs * f.nu * f.hw;
-      for (int e = lane; e < f.nu * f.hw; e += 32) {
-        const int rr = e / f.hw;
-        cpa16(reinterpret_cast<double2*>(PX) + rr * f.hwp + (e - rr * f.hw), srcx + e, true);
-      }
+      const double2* srcx = f.px_all + (size_t)kxs * f.nu * f.hwp;
+      for (int e = lane; e < f.nu * f.hwp; e += 32) cpa16(reinterpret_cast<double2*>(PX) + e, srcx + e, true);
     }
     cpa_commit();
   };
@@ -400,9 +436,13 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
       X[(I * 8 + q) * LD + 2 * t + 1] = r[I][1];
     }
     __syncwarp();
-    double* TT = S;  // S and T are contiguous: 2 * 64 doubles = t[0..63]
+    double* TT = X + NP * LD / 2;  // t[0..n-1] (complex) in X's upper half, E below it
     const int H8 = NBc * 8;
-    for (int rr = lane; rr < p.n; rr += 32) {
+    double tre[2] = {0.0, 0.0}, tim[2] = {0.0, 0.0};
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int rr = lane + 32 * it;
+      if (rr >= p.n) continue;
       double re, im;
       if (ODD && rr == h) {
         re = X[(2 * H8) * LD + 6];
@@ -415,8 +455,16 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
         re = X[pq * LD + 6] + X[(H8 + pq) * LD + 7];
         im = X[(H8 + pq) * LD + 6] - X[pq * LD + 7];
       }
-      TT[2 * rr] = re;
-      TT[2 * rr + 1] = im;
+      tre[it] = re;
+      tim[it] = im;
+    }
+    __syncwarp();  // every lane is done reading the RHS columns out of X
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int rr = lane + 32 * it;
+      if (rr >= p.n) continue;
+      TT[2 * rr] = tre[it];
+      TT[2 * rr + 1] = tim[it];
     }
     __syncwarp();
     // extended table E[k + n - 1] = t[k] for k in [-(n-1), n-1] (t[-k] = conj t[k]), in X
@@ -468,21 +516,18 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         if (q != 2 * t + e) continue;
-        const int col = I * 8 + q;
+        const double2 ab = RG[I * 8 + q];
         double add = 1.0;  // padding column: identity
-        if (MODE == MODE_SYMREAL) {
-          const bool cpart = I < NBc, spart = I >= NBc && I < 2 * NBc;
-          const int pp = cpart ? col : (spart ? col - NBc * 8 : h);
-          if ((cpart || spart) && pp < h) {
+        if (ab.x >= 0.0) {
+          const double r1 = __dadd_rn(__dmul_rn(w4, ab.x), p.eps);
+          if (ab.y >= 0.0) {
             // pair (p, n-1-p): lam (reg_p + reg_{n-1-p}) / 4 on the unscaled basis
-            const double r1 = __dadd_rn(__dmul_rn(w4, p.d4[pp]), p.eps);
-            const double r2 = __dadd_rn(__dmul_rn(w4, p.d4[p.n - 1 - pp]), p.eps);
-            add = p.lam > 0.0 ? __dmul_rn(p.lam, 0.25 * __dadd_rn(r1, r2)) : 0.0;
-          } else if (!cpart && !spart && ODD && q == 0) {
-            add = p.lam > 0.0 ? __dmul_rn(p.lam, __dadd_rn(__dmul_rn(w4, p.d4[h]), p.eps)) : 0.0;
+            const double r2 = __dadd_rn(__dmul_rn(w4, ab.y), p.eps);
+            add = __dmul_rn(p.lam, 0.25 * __dadd_rn(r1, r2));
+          } else {
+            add = __dmul_rn(p.lam, r1);
           }
-        } else if (col < p.n) {
-          add = p.lam > 0.0 ? __dmul_rn(p.lam, __dadd_rn(__dmul_rn(w4, p.d4[col]), p.eps)) : 0.0;
+          if (!(p.lam > 0.0)) add = 0.0;
         }
         g[blk(I, I)][e] = __dadd_rn(g[blk(I, I)][e], add);
       }
@@ -501,17 +546,17 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     const int Kb = PAIR && st < NBc ? NBc + st : -1;
     // (a) factor the diagonal block(s) with 8 lanes each (lane = row) and invert;
     //     column values are broadcast by shuffles, pivots by rsqrt.
-    store_c(S, g[blk(Ka, Ka)], lane);
-    if (Kb >= 0) store_c(T, g[blk(Kb, Kb)], lane);
+    store_cd(D0, g[blk(Ka, Ka)], lane);
+    if (Kb >= 0) store_cd(D1, g[blk(Kb, Kb)], lane);
     __syncwarp();
     bool lok = true;
     if (lane < 16) {
       const int hi = lane >> 3, row = lane & 7;
       const bool own = hi == 0 || Kb >= 0;  // lanes 8..15 of a one-block step repeat lanes 0..7
-      double* Sx = (hi && Kb >= 0) ? T : S;
+      double* Sx = (hi && Kb >= 0) ? D1 : D0;
       double a[8], dinv[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) a[c] = Sx[row * LD + c];
+      for (int c = 0; c < 8; ++c) a[c] = Sx[row * LDD + c];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const double akk = __shfl_sync(0xffffu, a[k], (lane & 8) | k);
@@ -526,7 +571,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
       __syncwarp(0xffffu);
       if (own) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) Sx[row * LD + c] = a[c];  // upper triangle ignored below
+        for (int c = 0; c < 8; ++c) Sx[row * LDD + c] = a[c];  // upper triangle ignored below
       }
       __syncwarp(0xffffu);
       // column `row` of W = L^-1: w_rr = (delta_rc - sum_{k<rr} L_rk w_k) / L_rr  (zero above c)
@@ -536,11 +581,11 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
       for (int rr = 0; rr < 8; ++rr) {
         double acc = (rr == c) ? 1.0 : 0.0;
 #pragma unroll
-        for (int k = 0; k < rr; ++k) acc = fma(-Sx[rr * LD + k], w[k], acc);
+        for (int k = 0; k < rr; ++k) acc = fma(-Sx[rr * LDD + k], w[k], acc);
         w[rr] = acc * dinv[rr];
       }
       if (own) {
-        double* Wd = Wst + (hi ? Kb : Ka) * 8 * LD;
+        double* Wd = Wblk(hi ? Kb : Ka);
 #pragma unroll
         for (int rr = 0; rr < 8; ++rr) Wd[rr * LD + c] = w[rr];
       }
@@ -551,7 +596,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     for (int side = 0; side < 2; ++side) {
       const int K = side ? Kb : Ka;
       if (K < 0) continue;
-      const double* Wk = Wst + K * 8 * LD;
+      const double* Wk = Wblk(K);
       // A-fragment of W (= B-fragment of W^T): W[q][t], W[q][4+t]
       const double wa0 = Wk[q * LD + t], wa1 = Wk[q * LD + 4 + t];
 
@@ -606,6 +651,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
   }
 
   // ---------------------------------------------------------------- 4. backward
+  bool finite = true;  // of the solution columns this lane holds
 #pragma unroll
   for (int K = NB - 1; K >= 0; --K) {
     double z[2] = {r[K][0], r[K][1]};
@@ -620,50 +666,44 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (NB <= 6 ? 2 : 1)))
     }
     store_c(T, z, lane);
     __syncwarp();
-    const double* Wk = Wst + K * 8 * LD;
+    const double* Wk = Wblk(K);
     const double at0 = Wk[t * LD + q], at1 = Wk[(4 + t) * LD + q];  // W^T A-fragment
     const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
     double x[2] = {0.0, 0.0};
     dmma(x, at0, b0);
     dmma(x, at1, b1);
+    finite = finite && (2 * t >= 2 * p.C || isfinite(x[0])) && (2 * t + 1 >= 2 * p.C || isfinite(x[1]));
     __syncwarp();
-    X[(K * 8 + q) * LD + 2 * t] = x[0];
-    X[(K * 8 + q) * LD + 2 * t + 1] = x[1];
+    *reinterpret_cast<double2*>(X + (K * 8 + q) * LD + 2 * t) = make_double2(x[0], x[1]);
+    // layer coefficients straight from this lane's solution entries (row K*8+q,
+    // channel t): the sin block of a (cos, sin) pair is solved first and read back here
+    if (t < p.C) {
+      const size_t cb = (size_t)t * plane + boff;
+      const size_t kst = (size_t)p.C * plane;
+      if (MODE == MODE_SYMREAL) {
+        const int pp = K * 8 + q;
+        if (K < NBc && pp < h) {
+          // v+ = aa + i bb, v- = cc + i dd;  x_p = (v+ + i v-)/2, x_{n-1-p} = (v+ - i v-)/2
+          const double2 sv = *reinterpret_cast<const double2*>(X + ((K + NBc) * 8 + q) * LD + 2 * t);
+          const double aa = x[0], bb = x[1], cc = sv.x, dd = sv.y;
+          p.layers[(size_t)pp * kst + cb] = make_float2((float)(0.5 * (aa - dd)), (float)(0.5 * (bb + cc)));
+          p.layers[(size_t)(p.n - 1 - pp) * kst + cb] = make_float2((float)(0.5 * (aa + dd)), (float)(0.5 * (bb - cc)));
+        } else if (ODD && K == NB - 1 && q == 0) {
+          p.layers[(size_t)h * kst + cb] = make_float2((float)x[0], (float)x[1]);
+        }
+      } else if (K * 8 + q < p.n) {
+        p.layers[(size_t)(K * 8 + q) * kst + cb] = make_float2((float)x[0], (float)x[1]);
+      }
+    }
     __syncwarp();
   }
 
   // ---------------------------------------------------------------- 5. output
-  bool finite = true;
-#pragma unroll
-  for (int e = 0; e < NP * 8 / 32; ++e) {
-    const int idx = e * 32 + lane;
-    if ((idx & 7) < 2 * p.C) finite = finite && isfinite(X[(idx >> 3) * LD + (idx & 7)]);
-  }
   ok = __all_sync(FULL, finite) && ok;
   if (p.status && lane == 0) p.status[soff] = ok ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
-  const float nanf_ = __int_as_float(0x7fc00000);
-  for (int e = lane; e < p.n * p.C; e += 32) {
-    const int k = e / p.C, c = e % p.C;
-    double xr, xi;
-    if (MODE == MODE_SYMREAL) {
-      const int H8 = NBc * 8;
-      if (ODD && k == h) {
-        xr = X[(2 * H8) * LD + 2 * c];
-        xi = X[(2 * H8) * LD + 2 * c + 1];
-      } else {
-        const bool hi = k >= h;
-        const int pp = hi ? p.n - 1 - k : k;
-        // v+ = aa + i bb, v- = cc + i dd;  x_p = (v+ + i v-)/2, x_{n-1-p} = (v+ - i v-)/2
-        const double aa = X[pp * LD + 2 * c], bb = X[pp * LD + 2 * c + 1];
-        const double cc = X[(H8 + pp) * LD + 2 * c], dd = X[(H8 + pp) * LD + 2 * c + 1];
-        xr = 0.5 * (hi ? aa + dd : aa - dd);
-        xi = 0.5 * (hi ? bb - cc : bb + cc);
-      }
-    } else {
-      xr = X[k * LD + 2 * c];
-      xi = X[k * LD + 2 * c + 1];
-    }
-    p.layers[((size_t)k * p.C + c) * plane + boff] = ok ? make_float2((float)xr, (float)xi) : make_float2(nanf_, nanf_);
+  if (!ok) {  // breakdown (rare): the bin's layers become NaN (overwriting what backward stored)
+    const float nanf_ = __int_as_float(0x7fc00000);
+    for (int e = lane; e < p.n * p.C; e += 32) p.layers[(size_t)e * plane + boff] = make_float2(nanf_, nanf_);
   }
   }  // bins of this warp
 }
@@ -673,8 +713,8 @@ int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
   const int ro_words = (MODE == MODE_SYMREAL) ? 2 * ((p.mrow + 3) & ~3) : 3 * p.m * p.n;
-  const size_t smem = sizeof(double) * ((size_t)py_words + ro_words +
-                                        (size_t)WARPS * (px_words + 16 * LD + NB * 8 * LD + NB * 8 * LD + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
+  const size_t smem = sizeof(double) * ((size_t)py_words + ro_words + 1 + 2 * NB * 8 +
+                                        (size_t)WARPS * (px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + NB * 8 * LD + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
   if (smem > 220 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
   auto kern = k1_fast_kernel<NB, MODE, ODD, PAIR>;
   FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -780,8 +820,8 @@ int k1_fast_launch(const SolveParams& p, cudaStream_t st, bool* handled) {
   *handled = true;
   if (p.mode == MODE_SYMREAL) {
     f.px_all = reinterpret_cast<const double2*>(p.fast_tables);
-    f.py_all = f.px_all + (size_t)p.Whp * f.nu * f.hw;
-    const long long tot = ((long long)p.Whp * f.nu + (long long)p.nrows * f.nv) * f.hw;
+    f.py_all = f.px_all + (size_t)p.Whp * f.nu * f.hwp;
+    const long long tot = ((long long)p.Whp * f.nu + (long long)p.nrows * f.nv) * f.hwp;
     int blocks = (int)std::min<long long>((tot + 255) / 256, 148LL * 8);
     k1_axis_tables_kernel<<<blocks, 256, 0, st>>>(p, f);
     FDL_LAUNCH_CHECK("k1_axis_tables_kernel");
