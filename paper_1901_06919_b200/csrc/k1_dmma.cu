@@ -89,7 +89,7 @@ __device__ __forceinline__ void store_c(double* S, const double (&c)[2], int lan
 // second block's scratch starts an odd number of doubles later, so the two
 // 8-lane groups of a paired step never share a bank either.
 constexpr int LDD = 9;
-constexpr int DSZ = 8 * LDD + 1;
+constexpr int DSZ = 8 * LDD;  // D1 - D0 = 144 words = 16 (mod 32): the complementary banks
 __device__ __forceinline__ void store_cd(double* D, const double (&c)[2], int lane) {
   const int q = lane >> 2, t = lane & 3;
   D[q * LDD + 2 * t] = c[0];
@@ -165,9 +165,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
 
   // shared layout: [PY: nv*hwp complex | ROW4 | RG] then per warp
   // [PX: nu*hwp complex | D 2*73 | S 64 | Wst (NB-1)*64 | X NP*8 | BS].  Lifetimes let
-  // buffers double up: T (the forward / backward 8x8 scratch) is X's first
-  // block, the W = L^-1 of the last diagonal block lives in S, and the
-  // Toeplitz build keeps t[] in X's upper half and E in its lower half.
+  // buffers double up: the W = L^-1 of the last diagonal block lives in S, and
+  // the Toeplitz build keeps t[] in X's upper half and E in its lower half.
   double* PY = smem;
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
@@ -190,7 +189,6 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
   double* S = D1 + DSZ;
   double* Wst = S + 8 * LD;
   double* X = Wst + (NB - 1) * 8 * LD;
-  double* T = X;
   // W = L_KK^-1 of diagonal block K
   auto Wblk = [&](int K) { return K == NB - 1 ? S : Wst + K * 8 * LD; };
   float2* BS = reinterpret_cast<float2*>(X + NP * LD);
@@ -511,11 +509,12 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
     // reference rounding: ((wx^2 + wy^2)^2 * d^4 + eps), G += lam * reg (construct.py:283,194)
     const double osq = __dadd_rn(__dmul_rn(ox, ox), __dmul_rn(oy, oy));
     const double w4 = __dmul_rn(osq, osq);
+    // lane (q, t) holds diagonal entry (q, q) of each diagonal block iff q >> 1 == t
+    const bool dlane = (q >> 1) == t;
+    const int e = q & 1;
 #pragma unroll
     for (int I = 0; I < NB; ++I) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (q != 2 * t + e) continue;
+      if (dlane) {
         const double2 ab = RG[I * 8 + q];
         double add = 1.0;  // padding column: identity
         if (ab.x >= 0.0) {
@@ -529,7 +528,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
           }
           if (!(p.lam > 0.0)) add = 0.0;
         }
-        g[blk(I, I)][e] = __dadd_rn(g[blk(I, I)][e], add);
+        if (e) g[blk(I, I)][1] = __dadd_rn(g[blk(I, I)][1], add);
+        else g[blk(I, I)][0] = __dadd_rn(g[blk(I, I)][0], add);
       }
     }
   }
@@ -624,21 +624,16 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
           dmma(g[blk(I, J)], -lf[I][1], lf[J][1]);
         }
       // (d) forward substitution: y_K = W r_K; r_I -= L_IK y_K
-      store_c(T, r[K], lane);
-      __syncwarp();
+      //     (accumulator -> B fragment by shuffles: C[t][q], C[4+t][q])
       {
-        const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
+        double b0, b1;
+        c_to_at(r[K], b0, b1, lane);
         double y[2] = {0.0, 0.0};
         dmma(y, wa0, b0);
         dmma(y, wa1, b1);
         r[K][0] = y[0];
         r[K][1] = y[1];
-      }
-      __syncwarp();
-      store_c(T, r[K], lane);
-      __syncwarp();
-      {
-        const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
+        c_to_at(y, b0, b1, lane);
 #pragma unroll
         for (int I = K + 1; I < NB; ++I) {
           if (!linked(I, K)) continue;
@@ -646,12 +641,13 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
           dmma(r[I], -lf[I][1], b1);
         }
       }
-      __syncwarp();
     }
   }
 
   // ---------------------------------------------------------------- 4. backward
   bool finite = true;  // of the solution columns this lane holds
+  double xa[NB][2];    // solved blocks, accumulator layout (the sin half waits for its cos partner)
+  double xb[NB][2];    // solved blocks as B fragments (x[t][q], x[4+t][q])
 #pragma unroll
   for (int K = NB - 1; K >= 0; --K) {
     double z[2] = {r[K][0], r[K][1]};
@@ -660,23 +656,22 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
       if (!linked(I, K)) continue;
       double a0, a1;
       c_to_at(g[blk(I, K)], a0, a1, lane);  // L_IK^T
-      const double b0 = X[(I * 8 + t) * LD + q], b1 = X[(I * 8 + 4 + t) * LD + q];
-      dmma(z, -a0, b0);
-      dmma(z, -a1, b1);
+      dmma(z, -a0, xb[I][0]);
+      dmma(z, -a1, xb[I][1]);
     }
-    store_c(T, z, lane);
-    __syncwarp();
+    double b0, b1;
+    c_to_at(z, b0, b1, lane);
     const double* Wk = Wblk(K);
     const double at0 = Wk[t * LD + q], at1 = Wk[(4 + t) * LD + q];  // W^T A-fragment
-    const double b0 = T[t * LD + q], b1 = T[(4 + t) * LD + q];
     double x[2] = {0.0, 0.0};
     dmma(x, at0, b0);
     dmma(x, at1, b1);
     finite = finite && (2 * t >= 2 * p.C || isfinite(x[0])) && (2 * t + 1 >= 2 * p.C || isfinite(x[1]));
-    __syncwarp();
-    *reinterpret_cast<double2*>(X + (K * 8 + q) * LD + 2 * t) = make_double2(x[0], x[1]);
+    xa[K][0] = x[0];
+    xa[K][1] = x[1];
+    c_to_at(x, xb[K][0], xb[K][1], lane);
     // layer coefficients straight from this lane's solution entries (row K*8+q,
-    // channel t): the sin block of a (cos, sin) pair is solved first and read back here
+    // channel t): the sin block of a (cos, sin) pair is solved first
     if (t < p.C) {
       const size_t cb = (size_t)t * plane + boff;
       const size_t kst = (size_t)p.C * plane;
@@ -684,8 +679,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
         const int pp = K * 8 + q;
         if (K < NBc && pp < h) {
           // v+ = aa + i bb, v- = cc + i dd;  x_p = (v+ + i v-)/2, x_{n-1-p} = (v+ - i v-)/2
-          const double2 sv = *reinterpret_cast<const double2*>(X + ((K + NBc) * 8 + q) * LD + 2 * t);
-          const double aa = x[0], bb = x[1], cc = sv.x, dd = sv.y;
+          const double aa = x[0], bb = x[1], cc = xa[K + NBc][0], dd = xa[K + NBc][1];
           p.layers[(size_t)pp * kst + cb] = make_float2((float)(0.5 * (aa - dd)), (float)(0.5 * (bb + cc)));
           p.layers[(size_t)(p.n - 1 - pp) * kst + cb] = make_float2((float)(0.5 * (aa + dd)), (float)(0.5 * (bb - cc)));
         } else if (ODD && K == NB - 1 && q == 0) {
@@ -695,7 +689,6 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
         p.layers[(size_t)(K * 8 + q) * kst + cb] = make_float2((float)x[0], (float)x[1]);
       }
     }
-    __syncwarp();
   }
 
   // ---------------------------------------------------------------- 5. output
