@@ -778,17 +778,20 @@ __global__ void __launch_bounds__(32 * TY, MINB) render_horner(RenderParams p) {
 // ---------------------------------------------------------------------------
 constexpr int H2_RING = 8;
 
+// One thread per (bin, VB views): the CTA's 128 threads take 128 consecutive
+// bins of the flattened (ky, kx) half spectrum (no column padding of a 2-D tile).
 template <int C, int VB>
 __global__ void __launch_bounds__(128, 4) render_horner2(RenderParams p) {
   __shared__ __align__(16) float2 LR[H2_RING][C][128];
   __shared__ __align__(16) u64 ZC[VB][128];  // block multipliers (used once per 8 layers)
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  const int kx = blockIdx.y * 32 + tx, ky = blockIdx.z * 4 + ty;
+  const int tid = threadIdx.x;
   const int v0 = blockIdx.x * VB;
   const int nv = min(VB, p.V - v0);
   const long long Q = (long long)p.Hp * p.Whp;
-  const bool inside = kx < p.Whp && ky < p.Hp;
-  const long long q = inside ? (long long)ky * p.Whp + kx : 0;
+  const long long qt = (long long)blockIdx.y * 128 + tid;
+  const bool inside = qt < Q;
+  const long long q = inside ? qt : 0;
+  const int ky = (int)(q / p.Whp), kx = (int)(q - (long long)ky * p.Whp);
   const int n = p.n;
   const int nb = (n + HB - 1) / HB;
 
@@ -880,21 +883,41 @@ __global__ void __launch_bounds__(128, 4) render_horner2(RenderParams p) {
   }
 }
 
+// views per thread: the largest register budget at 4 CTAs/SM (VB), or one of
+// the two next smaller counts when that pads fewer views (162 = 18 x 9 on C2)
 template <int C> struct H2VB;
 template <> struct H2VB<1> { static constexpr int vb = 16; };
 template <> struct H2VB<2> { static constexpr int vb = 12; };
 template <> struct H2VB<3> { static constexpr int vb = 10; };
 template <> struct H2VB<4> { static constexpr int vb = 8; };
 
+template <int C, int VB>
+int launch_horner2_vb(const RenderParams& p, cudaStream_t st) {
+  const long long Q = (long long)p.Hp * p.Whp;
+  dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((Q + 127) / 128));
+  render_horner2<C, VB><<<grid, 128, 0, st>>>(p);
+  FDL_LAUNCH_CHECK("render_horner2");
+  return FDL_OK;
+}
+
 template <int C>
 int launch_horner2(const RenderParams& p, cudaStream_t st) {
   render_z_kernel<<<p.V, 256, 0, st>>>(p);
   FDL_LAUNCH_CHECK("render_z_kernel");
   constexpr int VB = H2VB<C>::vb;
-  dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((p.Whp + 31) / 32), (unsigned)((p.Hp + 3) / 4));
-  render_horner2<C, VB><<<grid, 128, 0, st>>>(p);
-  FDL_LAUNCH_CHECK("render_horner2");
-  return FDL_OK;
+  int best = VB;
+  long long pad = (long long)((p.V + VB - 1) / VB) * VB;
+  for (int vb = VB - 1; vb >= VB - 2; --vb) {
+    const long long pv = (long long)((p.V + vb - 1) / vb) * vb;
+    if (pv < pad) {
+      pad = pv;
+      best = vb;
+    }
+  }
+  if (const char* e = getenv("FDL_H2_VB")) best = std::max(VB - 2, std::min(VB, atoi(e)));
+  if (best == VB) return launch_horner2_vb<C, VB>(p, st);
+  if (best == VB - 1) return launch_horner2_vb<C, VB - 1>(p, st);
+  return launch_horner2_vb<C, VB - 2>(p, st);
 }
 
 // ---------------------------------------------------------------------------
