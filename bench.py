@@ -206,6 +206,120 @@ def run_c5(args, rank, world, device):
             "clocks": clocks, "gpu_launches": args.steps * 4 * math.ceil(per_step / dev_batch)}
 
 
+def calib_flops_per_bin(m: int, n: int, grad: bool) -> float:
+    """fp64 flops of one calibration bin evaluation (calibrate.py:139-229): Hermitian
+    Gram 4mn(n+1), RHS 8mn, Cholesky (4/3)n^3, two solves 8n^2, residual 8mn,
+    Gamma x 2n^2 (+ gradient 8mn); the phase generation is not counted."""
+    return 4 * m * n * (n + 1) + 8 * m * n + (4.0 / 3.0) * n ** 3 + 8 * n * n + 8 * m * n + 2 * n * n + (
+        8 * m * n if grad else 0)
+
+
+CALIB_BATCH = 4096  # CalibConfig.batch_size default (calibrate.py:65)
+
+
+def calib_case(args, device):
+    """Calibration workload: the config-2 light field (81 views 512x512 RGB), 30 layers,
+    one descent iteration = the gradient evaluation + one backtracking trial over a
+    4096-bin batch of the frequency pool (calibrate.py:378-392)."""
+    from harness.synth import make_case
+    case = make_case("c2", args.size, device=device)
+    rng = np.random.default_rng(7)
+    m, n = len(case.u), len(case.d)
+    u = case.u + 0.02 * rng.standard_normal(m)
+    v = case.v + 0.02 * rng.standard_normal(m)
+    return case, np.outer(u, case.d), np.outer(v, case.d), rng
+
+
+def run_calib(args, device):
+    """--config calib: GPU calibration iterations (paper_1901_06919_b200.calibrate, K5)."""
+    import torch
+    import paper_1901_06919_b200 as fdl
+    import importlib
+    CAL = importlib.import_module("paper_1901_06919_b200.calibrate")
+    case, pu, pv, rng = calib_case(args, device)
+    m, H, W, C = case.views.shape
+    n = pu.shape[1]
+    views = fdl.ViewSet(images=case.views.cpu().numpy(), u=case.u, v=case.v)
+    spectra = CAL._Spectra(views)
+    pool = CAL.frequency_pool(spectra.grid)
+    spectra.normalise(pool)
+    eng = CAL._Engine(spectra, n, CAL.layer_regularizer(n), CAL.DEFAULT_LAMBDA)
+    batches = [np.sort(rng.permutation(pool)[:CALIB_BATCH]) for _ in range(4)]
+    trial_pu, trial_pv = pu * 1.001, pv * 1.001
+
+    def step(i):
+        sel = batches[i % len(batches)]
+        eng.batch_objective(pu, pv, sel, grad=True)
+        eng.batch_objective(trial_pu, trial_pv, sel)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(device.index or 0)
+    sampler.start()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    t = e0.elapsed_time(e1) / 1e3 / args.steps
+    # kernel-only time of one evaluation pair (solve + terms), CUDA events around the launches
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sel = batches[0]
+    k0.record(stream)
+    eng.solve(pu, pv, sel)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    ts = k0.elapsed_time(k1) / 1e3
+    flops = CALIB_BATCH * (calib_flops_per_bin(m, n, True) + calib_flops_per_bin(m, n, False))
+    dfma_peak = 34.2
+    res = {"metric": "calibration descent: frequency-bin evaluations/s (config-2 views)",
+           "value": 2 * CALIB_BATCH / t, "unit": "bin-evaluations/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (harness/synth.py config-2 light field, perturbed grid coordinates)",
+           "config": {"workload": f"calib: {m} views {H}x{W}x{C} (luminance), n={n} layers, one descent iteration = "
+                                  f"gradient + one trial evaluation of a {CALIB_BATCH}-bin batch",
+                      "batch": CALIB_BATCH, "l2": "spectra (Q x m complex128, 170 MB) exceed L2"},
+           "solve_ms": 1e3 * ts,
+           "roofline": {"bound": "fp64", "kernel": "K5 calibration solve + terms (DFMA)",
+                        "achieved": flops / t / 1e12, "peak": dfma_peak, "unit": "TFLOP/s",
+                        "frac": flops / t / 1e12 / dfma_peak,
+                        "peak_source": "measured DFMA (tools/microbench/fp64_pipes.cu)",
+                        "note": "step time includes the host descent bookkeeping and one device->host read per evaluation"},
+           "clocks": clocks, "gpu_launches": args.steps * 2 * 4,
+           "e2e": {"value": 2 * CALIB_BATCH / t, "unit": "bin-evaluations/s",
+                   "h2d_bytes_per_step": 2 * (CALIB_BATCH * 4 + 2 * m * n * 8),
+                   "d2h_bytes_per_step": 2 * 8 + 2 * m * n * 8}}
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = calib_cpu(args, case, pu, pv, batches[0])
+    return res
+
+
+def calib_cpu(args, case, pu, pv, sel, steps=1):
+    """The reference's batch evaluation (oracle restatement of calibrate.py:139-229) on the host."""
+    from oracle import fdl_oracle as O
+    imgs = case.views.cpu().numpy().astype(np.float64)
+    m, H, W, C = imgs.shape
+    n = pu.shape[1]
+    spec = O.luma_spectra(imgs)
+    gamma = O.layer_regularizer(n)
+    sample = sel[:512]
+    c0, w0 = time.process_time(), time.perf_counter()
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.calib_batch(pu, pv, spec, sample, W, H, 1e-3, gamma, grad=True)
+        O.calib_batch(pu * 1.001, pv * 1.001, spec, sample, W, H, 1e-3, gamma)
+        ts.append(time.perf_counter() - t0)
+    cores = (time.process_time() - c0) / max(time.perf_counter() - w0, 1e-9)
+    return {"value": 2 * len(sample) / float(np.mean(ts)), "unit": "bin-evaluations/s", "cores": round(cores, 2),
+            "kind": "port", "sample": f"gradient + trial evaluation of {len(sample)} of the batch's bins"}
+
+
 def run_ours(args, rank, world, device):
     import torch
     import torch.distributed as dist
@@ -460,6 +574,17 @@ def run_reference(args):
     if rank != 0:
         return None
     dev = "cpu"
+    if args.config == "calib":
+        case, pu, pv, rng = calib_case(args, dev)
+        sel = np.sort(rng.permutation(np.arange(case.views.shape[1] * (case.views.shape[2] // 2 + 1)))[:CALIB_BATCH])
+        cb = calib_cpu(args, case, pu, pv, sel, steps=max(1, args.steps))
+        return {"impl": "reference", "metric": "calibration descent: frequency-bin evaluations/s (config-2 views)",
+                "value": cb["value"], "unit": cb["unit"], "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * 2 * 512 / cb["value"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "calib (oracle port of calibrate.py:139-229)", "batch": 512},
+                "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     case = make_workload(args.config, args.size, dev)
     m, H, W, C = case.views.shape
     n = len(case.d)
@@ -512,6 +637,10 @@ def main():
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=device)
+    if args.config == "calib":
+        if rank == 0:
+            print(json.dumps(run_calib(args, device)))
+        return
     if args.config == "c5":
         res = run_c5(args, rank, world, device)
         if rank == 0:

@@ -171,6 +171,47 @@ typedef struct fdl_dense_desc {
 size_t fdl_solve_dense_workspace(const fdl_dense_desc* desc);
 int fdl_solve_dense(const fdl_dense_desc* desc, void* workspace_dev, size_t workspace_bytes, void* stream);
 
+/* Minimum-norm least squares x = lstsq(A, b) per problem (numpy's rcond=None
+ * cutoff), fp64 one-sided Jacobi SVD: the reference's degenerate-case
+ * fallback in the calibration solve (calibrate.py:164-169, lstsq(G, rhs)).
+ * A (batch, rows, n), b (batch, rows, C), x (batch, n, C) complex128;
+ * status (batch): 2 solved (the dense API's "minimum-norm solution" code), 1 failed. */
+size_t fdl_lstsq_minnorm_workspace(int32_t batch, int32_t rows, int32_t n, int32_t C);
+int fdl_lstsq_minnorm(int32_t batch, int32_t rows, int32_t n, int32_t C, const void* A_dev, const void* b_dev,
+                      void* x_dev, int8_t* status_dev, void* workspace_dev, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Calibration batches   (calibrate.py:139-229)                             */
+/* ------------------------------------------------------------------------ */
+
+/* One stochastic-descent evaluation over B frequency bins of the (unpadded)
+ * luminance spectra: A_jk = exp(2 pi i (Pu_jk wx + Pv_jk wy)) with the
+ * reference's phase rounding (`_system_batch`, calibrate.py:139-141),
+ * x = (A^H A + lam Gamma^T Gamma)^-1 A^H b (`_solve_batch`, :157-170),
+ * objective sum |A x - b|^2 + lam |Gamma x|^2 (`_objective_terms`, :172-178)
+ * and the shift-matrix gradients 4 pi sum_q w_q Im(conj(x_qk) conj(A_qjk) r_qj)
+ * (`_grad_p`, :219-229), summed over the batch in a fixed order. */
+typedef struct fdl_calib_desc {
+  int32_t m, n, B;            /* views, layers (<= 64), bins in this batch */
+  int32_t H, W;               /* spectrum grid: H rows x (W/2 + 1) stored columns */
+  const int32_t* bins;        /* host, B: flat stored-bin indices ky * (W/2+1) + kx */
+  const double* pu;           /* host, (m, n) */
+  const double* pv;           /* host, (m, n) */
+  const double* gamma;        /* host, (n, n) the layer regulariser Gamma (calibrate.py:113-123) */
+  double lam;                 /* >= 0 */
+  const void* spec_dev;       /* (H * (W/2+1), m) complex128 luminance spectra */
+  void* x_dev;                /* (B, n) complex128: written by _solve, read by _terms */
+  int8_t* status_dev;         /* (B): 0 solved, 2 Cholesky breakdown (G, rhs left for the fallback) */
+  void* gfall_dev;            /* (B, n, n) complex128: G of flagged bins */
+  void* rfall_dev;            /* (B, n) complex128: rhs of flagged bins */
+  double* obj_dev;            /* (1): sum of the batch's objective terms (_terms) */
+  double* grad_dev;           /* (2, m, n): gradients w.r.t. Pu and Pv summed over the batch, or NULL */
+} fdl_calib_desc;
+
+size_t fdl_calib_workspace(const fdl_calib_desc* desc);
+int fdl_calib_solve(const fdl_calib_desc* desc, void* workspace_dev, size_t workspace_bytes, void* stream);
+int fdl_calib_terms(const fdl_calib_desc* desc, void* workspace_dev, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* K2: conjugate-pair symmetrisation of self-conjugate columns (construct.py:286-297) */
 /* ------------------------------------------------------------------------ */

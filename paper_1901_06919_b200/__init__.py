@@ -4,8 +4,10 @@ Drop-in for the reference package `fdl` on these paths (same names, argument
 meaning and exceptions as fdl/__init__.py:3-98 for everything below); the
 compute runs in hand-written sm_100a CUDA kernels behind a C ABI
 (include/fdl_b200.h, libfdl_b200.so).  FDL1 model files are read and
-written straight from / into device memory (io.py).
-Out of scope: calibration, pipelines, CLI, HTTP service, viewer.
+written straight from / into device memory (io.py, SURVEY.md §8(f) row 3);
+calibration runs its batch solves, objective and gradients on the GPU
+(calibrate.py).
+Out of scope: pipelines, CLI, HTTP service, viewer.
 """
 
 from .spectra import DFT_CONVENTION, FrequencyGrid
@@ -34,10 +36,34 @@ from .render import (
 )
 
 from .io import ModelFormatError, load_model, save_model
+from .calibrate import (
+    CalibConfig,
+    CalibrationDivergence,
+    CalibrationResult,
+    calibrate,
+    calibrate_relaxed,
+    grad_factored,
+    grad_shift_matrix,
+    layer_coefficients,
+    layer_regularizer,
+    objective,
+    regauge_to_coords,
+)
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "CalibConfig",
+    "CalibrationDivergence",
+    "CalibrationResult",
+    "calibrate",
+    "calibrate_relaxed",
+    "grad_factored",
+    "grad_shift_matrix",
+    "layer_coefficients",
+    "layer_regularizer",
+    "objective",
+    "regauge_to_coords",
     "DFT_CONVENTION",
     "FrequencyGrid",
     "GAMMA",

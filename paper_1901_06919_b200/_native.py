@@ -76,6 +76,18 @@ class FdlDenseDesc(ctypes.Structure):
     ]
 
 
+class FdlCalibDesc(ctypes.Structure):
+    _fields_ = [
+        ("m", ctypes.c_int32), ("n", ctypes.c_int32), ("B", ctypes.c_int32),
+        ("H", ctypes.c_int32), ("W", ctypes.c_int32),
+        ("bins", c_int32_p), ("pu", c_double_p), ("pv", c_double_p), ("gamma", c_double_p),
+        ("lam", ctypes.c_double),
+        ("spec_dev", ctypes.c_void_p), ("x_dev", ctypes.c_void_p), ("status_dev", ctypes.c_void_p),
+        ("gfall_dev", ctypes.c_void_p), ("rfall_dev", ctypes.c_void_p),
+        ("obj_dev", ctypes.c_void_p), ("grad_dev", ctypes.c_void_p),
+    ]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -97,6 +109,14 @@ EXPORTS = {
                                         ctypes.c_size_t, ctypes.c_void_p]),
     "fdl_solve_dense_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlDenseDesc)]),
     "fdl_solve_dense": (ctypes.c_int, [ctypes.POINTER(FdlDenseDesc), ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.c_void_p]),
+    "fdl_lstsq_minnorm_workspace": (ctypes.c_size_t, [ctypes.c_int32] * 4),
+    "fdl_lstsq_minnorm": (ctypes.c_int, [ctypes.c_int32] * 4 + [ctypes.c_void_p] * 4 + [
+        ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "fdl_calib_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlCalibDesc)]),
+    "fdl_calib_solve": (ctypes.c_int, [ctypes.POINTER(FdlCalibDesc), ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.c_void_p]),
+    "fdl_calib_terms": (ctypes.c_int, [ctypes.POINTER(FdlCalibDesc), ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p]),
     "fdl_symmetrize": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 5 + [
         c_int32_p, c_int32_p, ctypes.c_void_p]),

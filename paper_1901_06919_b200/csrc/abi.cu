@@ -34,6 +34,14 @@ int build_bins_launch(const SolveParams& p, const int* bins, int nb, double2* A,
                       cudaStream_t st);
 int scatter_bins_launch(const SolveParams& p, const int* bins, int nb, const double2* x, const signed char* st2,
                         cudaStream_t st);
+// --- k5_calib.cu -----------------------------------------------------------------
+size_t calib_solve_smem(int m, int n);
+size_t calib_terms_smem(int m, int n);
+int calib_terms_ctas(int B);
+int calib_launch(int m, int n, int B, int H, int W, const int* bins, const double* pu, const double* pv,
+                 const double2* spec, const double* gram, const double* gamma, double lam, double2* x,
+                 signed char* status, double2* gfall, double2* rfall, double* obj_bins, double* gpart,
+                 double* obj, double* grad, bool solve, bool terms, cudaStream_t st);
 
 // --- errors --------------------------------------------------------------------
 thread_local std::string t_error;
@@ -809,6 +817,97 @@ int fdl_resolve_bins(const fdl_solve_desc* desc, const int32_t* bins, int32_t nb
                           reinterpret_cast<double*>(ws + L.scratch), true, st);
   if (rc) return rc;
   return scatter_bins_launch(P.p, dbins, nbins, x, s2, st);
+}
+
+// ---------------------------------------------------------------- calibration
+namespace {
+struct CalibPlan {
+  Blob blob;
+  size_t o_bins, o_pu, o_pv, o_gram, o_gamma, o_objb, o_gpart;
+};
+int plan_calib(const fdl_calib_desc* d, CalibPlan& P) {
+  if (!d || d->m < 1 || d->n < 1 || d->B < 0 || d->H < 1 || d->W < 1) return fail(FDL_ERR_INVALID, "invalid calibration batch");
+  if (d->n > 64) return fail(FDL_ERR_UNSUPPORTED, "calibration supports n <= 64 layers");
+  if (!(d->lam >= 0.0) || !std::isfinite(d->lam)) return fail(FDL_ERR_INVALID, "lam must be non-negative");
+  if (!d->bins || !d->pu || !d->pv || !d->gamma) return fail(FDL_ERR_INVALID, "null host array");
+  const int Q = d->H * (d->W / 2 + 1), m = d->m, n = d->n;
+  for (int i = 0; i < d->B; ++i)
+    if (d->bins[i] < 0 || d->bins[i] >= Q) return fail(FDL_ERR_INVALID, "frequency index out of range");
+  if (!finite_all(d->pu, (size_t)m * n) || !finite_all(d->pv, (size_t)m * n))
+    return fail(FDL_ERR_INVALID, "shift parameters must be finite");
+  std::vector<double> gram((size_t)n * n, 0.0);  // Gamma^T Gamma (calibrate.py:334)
+  for (int k = 0; k < n; ++k)
+    for (int l = 0; l < n; ++l) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s += d->gamma[(size_t)i * n + k] * d->gamma[(size_t)i * n + l];
+      gram[(size_t)k * n + l] = s;
+    }
+  Blob& B = P.blob;
+  P.o_bins = B.add(d->bins, sizeof(int) * std::max(d->B, 1));
+  P.o_pu = B.add(d->pu, sizeof(double) * m * n);
+  P.o_pv = B.add(d->pv, sizeof(double) * m * n);
+  P.o_gram = B.add(gram.data(), sizeof(double) * n * n);
+  P.o_gamma = B.add(d->gamma, sizeof(double) * n * n);
+  P.o_objb = B.reserve(sizeof(double) * std::max(d->B, 1));
+  P.o_gpart = B.reserve(sizeof(double) * 2 * (size_t)m * n * calib_terms_ctas(d->B));
+  return FDL_OK;
+}
+int run_calib(const fdl_calib_desc* d, void* ws, size_t wsb, void* stream, bool solve, bool terms) {
+  CalibPlan P;
+  int rc = plan_calib(d, P);
+  if (rc) return rc;
+  if (!ws || wsb < P.blob.size()) return fail(FDL_ERR_INVALID, "workspace too small for the calibration batch");
+  if (!d->spec_dev || !d->x_dev || !d->status_dev) return fail(FDL_ERR_INVALID, "null device buffer");
+  if (solve && (!d->gfall_dev || !d->rfall_dev)) return fail(FDL_ERR_INVALID, "null fallback buffer");
+  if (terms && !d->obj_dev) return fail(FDL_ERR_INVALID, "null objective buffer");
+  cudaStream_t st = as_stream(stream);
+  // the upload block ends before the device-only scratch (objective terms, partials)
+  Blob up = P.blob;
+  up.bytes.resize(P.o_objb);
+  if ((rc = upload(up, ws, st))) return rc;
+  return calib_launch(d->m, d->n, d->B, d->H, d->W, at<int>(ws, P.o_bins), at<double>(ws, P.o_pu),
+                      at<double>(ws, P.o_pv), reinterpret_cast<const double2*>(d->spec_dev), at<double>(ws, P.o_gram),
+                      at<double>(ws, P.o_gamma), d->lam, reinterpret_cast<double2*>(d->x_dev), d->status_dev,
+                      reinterpret_cast<double2*>(d->gfall_dev), reinterpret_cast<double2*>(d->rfall_dev),
+                      const_cast<double*>(at<double>(ws, P.o_objb)),
+                      d->grad_dev ? const_cast<double*>(at<double>(ws, P.o_gpart)) : nullptr, d->obj_dev, d->grad_dev,
+                      solve, terms, st);
+}
+}  // namespace
+
+size_t fdl_calib_workspace(const fdl_calib_desc* d) {
+  CalibPlan P;
+  if (plan_calib(d, P)) return 0;
+  return P.blob.size();
+}
+
+int fdl_calib_solve(const fdl_calib_desc* d, void* ws, size_t wsb, void* stream) {
+  return run_calib(d, ws, wsb, stream, true, false);
+}
+
+int fdl_calib_terms(const fdl_calib_desc* d, void* ws, size_t wsb, void* stream) {
+  return run_calib(d, ws, wsb, stream, false, true);
+}
+
+size_t fdl_lstsq_minnorm_workspace(int32_t batch, int32_t rows, int32_t n, int32_t C) {
+  if (batch < 0 || rows < 1 || n < 1 || C < 1) return 0;
+  return align256(8 * (size_t)batch * dense_scratch_doubles(rows, n, C)) + align256(8 * (size_t)batch * n) + 256;
+}
+
+int fdl_lstsq_minnorm(int32_t batch, int32_t rows, int32_t n, int32_t C, const void* A_dev, const void* b_dev,
+                      void* x_dev, int8_t* status_dev, void* ws, size_t wsb, void* stream) {
+  if (batch < 0 || rows < 1 || n < 1 || C < 1) return fail(FDL_ERR_INVALID, "invalid least-squares batch");
+  if (!A_dev || !b_dev || !x_dev || !status_dev) return fail(FDL_ERR_INVALID, "null buffer");
+  if (!ws || wsb < fdl_lstsq_minnorm_workspace(batch, rows, n, C)) return fail(FDL_ERR_INVALID, "workspace too small");
+  if (batch == 0) return FDL_OK;
+  cudaStream_t st = as_stream(stream);
+  // min-norm solution of A x = b: the stacked solver with a zero regulariser
+  double* scratch = reinterpret_cast<double*>(ws);
+  double* zreg = scratch + align256(8 * (size_t)batch * dense_scratch_doubles(rows, n, C)) / 8;
+  FDL_CUDA_CHECK(cudaMemsetAsync(zreg, 0, 8 * (size_t)batch * n, st));
+  return dense_solve_launch(batch, rows, n, C, reinterpret_cast<const double2*>(A_dev),
+                            reinterpret_cast<const double2*>(b_dev), zreg, nullptr, 1.0,
+                            reinterpret_cast<double2*>(x_dev), status_dev, status_dev, scratch, true, st);
 }
 
 size_t fdl_solve_dense_workspace(const fdl_dense_desc* d) {

@@ -71,3 +71,25 @@ def test_solve_path_selection(d, u, expect):
     from paper_1901_06919_b200 import _native as nat
     desc, keep = _desc(2, len(d), d, u, [0.0, 0.0])
     assert nat.lib().fdl_solve_path(desc) == expect
+
+
+def test_calibration_entry_points_validate_without_gpu():
+    import ctypes
+    from paper_1901_06919_b200 import _native as nat
+    lib = nat.lib()
+    d = nat.FdlCalibDesc()
+    d.m, d.n, d.B, d.H, d.W = 2, 0, 4, 8, 8
+    assert lib.fdl_calib_workspace(ctypes.byref(d)) == 0
+    assert lib.fdl_calib_solve(ctypes.byref(d), None, 0, None) == nat.FDL_ERR_INVALID
+    # a valid plan needs host arrays; out-of-range bins are refused before any device work
+    bins = np.array([0, 1, 99], dtype=np.int32)
+    pu = np.zeros((2, 2))
+    gam = np.eye(2)
+    d.n, d.B = 2, 3
+    d.bins, d.pu, d.pv, d.gamma = nat.iptr(bins), nat.dptr(pu), nat.dptr(pu), nat.dptr(gam)
+    assert lib.fdl_calib_workspace(ctypes.byref(d)) == 0
+    assert b"out of range" in lib.fdl_last_error()
+    bins[2] = 5
+    assert lib.fdl_calib_workspace(ctypes.byref(d)) > 0
+    assert lib.fdl_lstsq_minnorm_workspace(2, 3, 3, 1) > 0
+    assert lib.fdl_lstsq_minnorm(-1, 3, 3, 1, None, None, None, None, None, 0, None) == nat.FDL_ERR_INVALID
