@@ -822,8 +822,8 @@ int fdl_resolve_bins(const fdl_solve_desc* desc, const int32_t* bins, int32_t nb
 // ---------------------------------------------------------------- calibration
 namespace {
 struct CalibPlan {
-  Blob blob;
-  size_t o_bins, o_pu, o_pv, o_gram, o_gamma, o_objb, o_gpart;
+  Blob blob;  // uploaded parameter block; the device-only scratch follows it
+  size_t o_bins, o_pu, o_pv, o_gram, o_gamma, o_objb, o_gpart, total;
 };
 int plan_calib(const fdl_calib_desc* d, CalibPlan& P) {
   if (!d || d->m < 1 || d->n < 1 || d->B < 0 || d->H < 1 || d->W < 1) return fail(FDL_ERR_INVALID, "invalid calibration batch");
@@ -848,23 +848,22 @@ int plan_calib(const fdl_calib_desc* d, CalibPlan& P) {
   P.o_pv = B.add(d->pv, sizeof(double) * m * n);
   P.o_gram = B.add(gram.data(), sizeof(double) * n * n);
   P.o_gamma = B.add(d->gamma, sizeof(double) * n * n);
-  P.o_objb = B.reserve(sizeof(double) * std::max(d->B, 1));
-  P.o_gpart = B.reserve(sizeof(double) * 2 * (size_t)m * n * calib_terms_ctas(d->B));
+  // device-only scratch (not part of the host image: no host allocation per call)
+  P.o_objb = B.size();
+  P.o_gpart = P.o_objb + align256(sizeof(double) * std::max(d->B, 1));
+  P.total = P.o_gpart + align256(sizeof(double) * 2 * (size_t)m * n * calib_terms_ctas(d->B));
   return FDL_OK;
 }
 int run_calib(const fdl_calib_desc* d, void* ws, size_t wsb, void* stream, bool solve, bool terms) {
   CalibPlan P;
   int rc = plan_calib(d, P);
   if (rc) return rc;
-  if (!ws || wsb < P.blob.size()) return fail(FDL_ERR_INVALID, "workspace too small for the calibration batch");
+  if (!ws || wsb < P.total) return fail(FDL_ERR_INVALID, "workspace too small for the calibration batch");
   if (!d->spec_dev || !d->x_dev || !d->status_dev) return fail(FDL_ERR_INVALID, "null device buffer");
   if (solve && (!d->gfall_dev || !d->rfall_dev)) return fail(FDL_ERR_INVALID, "null fallback buffer");
   if (terms && !d->obj_dev) return fail(FDL_ERR_INVALID, "null objective buffer");
   cudaStream_t st = as_stream(stream);
-  // the upload block ends before the device-only scratch (objective terms, partials)
-  Blob up = P.blob;
-  up.bytes.resize(P.o_objb);
-  if ((rc = upload(up, ws, st))) return rc;
+  if ((rc = upload(P.blob, ws, st))) return rc;
   return calib_launch(d->m, d->n, d->B, d->H, d->W, at<int>(ws, P.o_bins), at<double>(ws, P.o_pu),
                       at<double>(ws, P.o_pv), reinterpret_cast<const double2*>(d->spec_dev), at<double>(ws, P.o_gram),
                       at<double>(ws, P.o_gamma), d->lam, reinterpret_cast<double2*>(d->x_dev), d->status_dev,
@@ -878,7 +877,7 @@ int run_calib(const fdl_calib_desc* d, void* ws, size_t wsb, void* stream, bool 
 size_t fdl_calib_workspace(const fdl_calib_desc* d) {
   CalibPlan P;
   if (plan_calib(d, P)) return 0;
-  return P.blob.size();
+  return P.total;
 }
 
 int fdl_calib_solve(const fdl_calib_desc* d, void* ws, size_t wsb, void* stream) {

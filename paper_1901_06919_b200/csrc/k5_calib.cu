@@ -270,15 +270,24 @@ __global__ void __launch_bounds__(CT) calib_terms_kernel(CalibParams p) {
   }
 }
 
-// out[0] = sum of per-bin objective terms; grad[e] = 4 pi sum_cta partial[cta][e]
+// block 0: obj = sum of the per-bin objective terms (strided partial sums and a
+// shared-memory tree, a fixed order); blocks >= 1: grad[e] = 4 pi sum_cta partial[cta][e]
 __global__ void calib_reduce_kernel(const double* obj_bins, int B, const double* gpart, int nparts, int len,
                                     double* obj, double* grad) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e == len) {
+  if (blockIdx.x == 0) {
+    __shared__ double t[256];
     double s = 0.0;
-    for (int b = 0; b < B; ++b) s += obj_bins[b];
-    *obj = s;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) s += obj_bins[b];
+    t[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) t[threadIdx.x] += t[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) *obj = t[0];
+    return;
   }
+  const int e = (blockIdx.x - 1) * blockDim.x + threadIdx.x;
   if (e < len && gpart) {
     double s = 0.0;
     for (int c = 0; c < nparts; ++c) s += gpart[(size_t)c * len + e];
@@ -313,7 +322,7 @@ int calib_launch(int m, int n, int B, int H, int W, const int* bins, const doubl
     calib_terms_kernel<<<ctas, CT, smem, st>>>(p);
     FDL_LAUNCH_CHECK("calib_terms_kernel");
     const int len = 2 * m * n;
-    calib_reduce_kernel<<<(len + 1 + 255) / 256, 256, 0, st>>>(obj_bins, B, gpart, ctas, len, obj, grad);
+    calib_reduce_kernel<<<1 + (gpart ? (len + 255) / 256 : 0), 256, 0, st>>>(obj_bins, B, gpart, ctas, len, obj, grad);
     FDL_LAUNCH_CHECK("calib_reduce_kernel");
   }
   return FDL_OK;
