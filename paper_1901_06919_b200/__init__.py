@@ -6,8 +6,9 @@ compute runs in hand-written sm_100a CUDA kernels behind a C ABI
 (include/fdl_b200.h, libfdl_b200.so).  FDL1 model files are read and
 written straight from / into device memory (io.py, SURVEY.md §8(f) row 3);
 calibration runs its batch solves, objective and gradients on the GPU
-(calibrate.py).
-Out of scope: pipelines, CLI, HTTP service, viewer.
+(calibrate.py), and so do the interpolate / denoise
+pipelines built on it (pipeline.py, row 2).
+Out of scope: CLI, HTTP service, viewer.
 """
 
 from .spectra import DFT_CONVENTION, FrequencyGrid
@@ -49,10 +50,16 @@ from .calibrate import (
     objective,
     regauge_to_coords,
 )
+from .pipeline import PipelineConfig, QualityReport, denoise, interpolate_views, psnr
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "PipelineConfig",
+    "QualityReport",
+    "denoise",
+    "interpolate_views",
+    "psnr",
     "CalibConfig",
     "CalibrationDivergence",
     "CalibrationResult",
