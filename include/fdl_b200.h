@@ -91,6 +91,15 @@ int fdl_views_to_spectra(const float* views_dev, int32_t m, int32_t H, int32_t W
                          int32_t pad, fdl_c64* spectra_dev, double* view_sumsq_dev,
                          void* workspace_dev, size_t workspace_bytes, void* stream);
 
+/* fdl_views_to_spectra for sRGB-encoded views: every value is decoded to
+ * linear light (render.py:39-42 srgb_decode) as K0 loads it, so a caller
+ * gets the spectra of srgb_decode(views) -- what the reference builds from
+ * after load_lightfield(..., to_linear=True) (io.py:147-149) -- without a
+ * decoded copy of the views in HBM.  Same workspace as fdl_views_to_spectra. */
+int fdl_views_to_spectra_srgb(const float* views_dev, int32_t m, int32_t H, int32_t W, int32_t C,
+                              int32_t pad, fdl_c64* spectra_dev, double* view_sumsq_dev,
+                              void* workspace_dev, size_t workspace_bytes, void* stream);
+
 /* Gather whole frequency rows of view spectra into a contiguous slab:
  * dst (m, C, nrows, Whp) <- src (m, C, Hp, Whp)[..., rows[i], :].  Used to pack
  * the all-to-all send buffers of the multi-GPU path. */

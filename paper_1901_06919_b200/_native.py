@@ -98,6 +98,8 @@ EXPORTS = {
     "fdl_views_to_spectra_workspace": (ctypes.c_size_t, [ctypes.c_int32] * 5),
     "fdl_views_to_spectra": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 5 + [
         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "fdl_views_to_spectra_srgb": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 5 + [
+        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "fdl_gather_rows": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 4 + [
         ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]),
     "fdl_solve_bins_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlSolveDesc)]),

@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 from . import _native as nat
-from .lfmodel import FdlModel, ShiftParams, ViewSet, _is_torch
+from .lfmodel import GAMMA, LINEAR, FdlModel, ShiftParams, ViewSet, _is_torch
 from .spectra import FrequencyGrid
 
 __all__ = [
@@ -292,8 +292,9 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     return layers, n_bad, path
 
 
-def views_to_spectra(views_dev, pad):
-    """K0 on a (m,H,W,C) float32 CUDA tensor -> (spectra (m,C,Hp,Whp) c64, per-view sum|b|^2 (m) f64)."""
+def views_to_spectra(views_dev, pad, srgb: bool = False):
+    """K0 on a (m,H,W,C) float32 CUDA tensor -> (spectra (m,C,Hp,Whp) c64, per-view sum|b|^2 (m) f64).
+    srgb: the views are sRGB-encoded and are decoded to linear light as K0 loads them."""
     import torch
     m, H, W, C = views_dev.shape
     Hp, Wp = H + 2 * pad, W + 2 * pad
@@ -305,16 +306,16 @@ def views_to_spectra(views_dev, pad):
     if ws_bytes == 0:
         raise nat.FdlNativeError("fdl_views_to_spectra_workspace: " + L.fdl_last_error().decode())
     ws = nat.workspace(ws_bytes, device)
-    nat.check(L.fdl_views_to_spectra(views_dev.data_ptr(), m, H, W, C, pad, spectra.data_ptr(),
-                                     sumsq.data_ptr(), ws.data_ptr(), ws.numel(),
-                                     nat.stream_handle(device)), "fdl_views_to_spectra")
+    k0 = L.fdl_views_to_spectra_srgb if srgb else L.fdl_views_to_spectra
+    nat.check(k0(views_dev.data_ptr(), m, H, W, C, pad, spectra.data_ptr(),
+                 sumsq.data_ptr(), ws.data_ptr(), ws.numel(), nat.stream_handle(device)), "fdl_views_to_spectra")
     return spectra, sumsq
 
 
 UPLOAD_CHUNK_BYTES = 24 << 20
 
 
-def views_to_spectra_host(images, pad, device, chunk_bytes: int = UPLOAD_CHUNK_BYTES):
+def views_to_spectra_host(images, pad, device, chunk_bytes: int = UPLOAD_CHUNK_BYTES, srgb: bool = False):
     """K0 on HOST views with the upload overlapped: view chunks go host->device
     on a side stream while K0 transforms the previous chunk on the current
     stream.  Pinned torch input is copied directly; anything else passes
@@ -357,9 +358,9 @@ def views_to_spectra_host(images, pad, device, chunk_bytes: int = UPLOAD_CHUNK_B
             ev = torch.cuda.Event()
             ev.record(copy)
         compute.wait_event(ev)
-        nat.check(L.fdl_views_to_spectra(views_dev[j0].data_ptr(), j1 - j0, H, W, C, pad,
-                                         spectra[j0].data_ptr(), sumsq[j0:].data_ptr(), ws.data_ptr(),
-                                         ws.numel(), nat.stream_handle(device)), "fdl_views_to_spectra")
+        k0 = L.fdl_views_to_spectra_srgb if srgb else L.fdl_views_to_spectra
+        nat.check(k0(views_dev[j0].data_ptr(), j1 - j0, H, W, C, pad, spectra[j0].data_ptr(), sumsq[j0:].data_ptr(),
+                     ws.data_ptr(), ws.numel(), nat.stream_handle(device)), "fdl_views_to_spectra")
     for e in ring_ev:
         if e is not None:
             e.synchronize()  # the staging ring may be reused by the caching host allocator
@@ -404,7 +405,7 @@ def lambda_from_sumsq(view_sumsq, Q: int, m: int) -> float:
 
 def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None, eps: float = DEFAULT_EPS,
                   pad_margin: int | None = None, chunk: int = SOLVE_CHUNK, *, device=None,
-                  force_path: int = 0, eager_host: bool | None = None) -> FdlModel:
+                  force_path: int = 0, eager_host: bool | None = None, decode_srgb: bool = False) -> FdlModel:
     """Build the disparity-layer model by per-frequency solves (construct.py:219-308).
 
     Same arguments, defaults and exceptions as the reference.  `chunk` is
@@ -413,8 +414,13 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
     current); `force_path` pins the K1 formulation (testing).  `eager_host`
     (default: when the views came from host memory) reads the layers back to
     pinned host memory slab by slab while later slabs solve; the model's
-    `.layers` / `layers_host()` then need no further transfer.
+    `.layers` / `layers_host()` then need no further transfer.  `decode_srgb`
+    (gamma-encoded views only) builds the model in linear light, decoding
+    every value as K0 loads it: the reference's load_lightfield(...,
+    to_linear=True) + construct_fdl (io.py:147-149) without a decoded copy.
     """
+    if decode_srgb and views.color_space != GAMMA:
+        raise ValueError("decode_srgb needs gamma-encoded (sRGB) views")
     torch = _require_cuda()
     pu, pv, d = resolve_shifts(views, shifts)
     m = views.num_views
@@ -428,9 +434,9 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
     Hp, Wp = H + 2 * pad_margin, W + 2 * pad_margin
     grid = FrequencyGrid(width=Wp, height=Hp)
     if _is_torch(views.images) and views.images.is_cuda:
-        spectra, sumsq = views_to_spectra(_views_device(views.images, dev), pad_margin)
+        spectra, sumsq = views_to_spectra(_views_device(views.images, dev), pad_margin, srgb=decode_srgb)
     else:
-        spectra, sumsq = views_to_spectra_host(views.images, pad_margin, dev)
+        spectra, sumsq = views_to_spectra_host(views.images, pad_margin, dev, srgb=decode_srgb)
     if lam is None:
         lam = lambda_from_sumsq(sumsq.cpu().numpy(), grid.num_entries, m)
     if lam < 0:
@@ -459,7 +465,8 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
     if host is None:
         symmetrize(layers, Hp, Wp)
     model = FdlModel(disparities=d, layers=layers, grid=grid, width=W, height=H, pad_margin=pad_margin,
-                     color_space=views.color_space, calibration=shifts, lambda_used=float(lam))
+                     color_space=LINEAR if decode_srgb else views.color_space, calibration=shifts,
+                     lambda_used=float(lam))
     if host is not None:
         model._host_async = host
     return model

@@ -17,7 +17,7 @@ namespace fdl {
 // --- k0_spectra.cu / k1_*.cu -------------------------------------------------
 int views_to_spectra_ws(int m, int H, int W, int C, int pad, size_t* bytes);
 int views_to_spectra(const float* views, int m, int H, int W, int C, int pad, fdl_c64* spectra, double* view_sumsq,
-                     void* ws, size_t ws_bytes, cudaStream_t st);
+                     void* ws, size_t ws_bytes, cudaStream_t st, int srgb = 0);
 int gather_rows(const fdl_c64* src, int m, int C, int Hp, int Whp, const int* rows_dev, int nrows, fdl_c64* dst,
                 cudaStream_t st);
 int spectra_to_images_ws(int V, int C, int Hp, int Wp, size_t* bytes);
@@ -692,6 +692,15 @@ int fdl_views_to_spectra(const float* views_dev, int32_t m, int32_t H, int32_t W
   if (!views_dev || !spectra_dev) return fail(FDL_ERR_INVALID, "null buffer");
   return views_to_spectra(views_dev, m, H, W, C, pad, spectra_dev, view_sumsq_dev, workspace_dev, workspace_bytes,
                           as_stream(stream));
+}
+
+int fdl_views_to_spectra_srgb(const float* views_dev, int32_t m, int32_t H, int32_t W, int32_t C, int32_t pad,
+                              fdl_c64* spectra_dev, double* view_sumsq_dev, void* workspace_dev,
+                              size_t workspace_bytes, void* stream) {
+  if (m < 1 || H < 1 || W < 1 || C < 1 || pad < 0) return fail(FDL_ERR_INVALID, "invalid view stack shape");
+  if (!views_dev || !spectra_dev) return fail(FDL_ERR_INVALID, "null buffer");
+  return views_to_spectra(views_dev, m, H, W, C, pad, spectra_dev, view_sumsq_dev, workspace_dev, workspace_bytes,
+                          as_stream(stream), 1);
 }
 
 int fdl_gather_rows(const fdl_c64* src_dev, int32_t m, int32_t C, int32_t Hp, int32_t Whp, const int32_t* rows_dev,

@@ -29,6 +29,11 @@ namespace {
 
 using fft::Geo;
 
+// sRGB-encoded value -> linear light (render.py:39-42; fused into the K0 load)
+__device__ inline float srgb_dec_f(float x) {
+  return x <= 0.04045f ? x / 12.92f : powf((fmaxf(x, 0.04045f) + 0.055f) / 1.055f, 2.4f);
+}
+
 __device__ inline float srgb_enc_f(float x) {
   x = fmaxf(x, 0.f);
   return x <= 0.0031308f ? x * 12.92f : 1.055f * powf(x, 1.0f / 2.4f) - 0.055f;
@@ -61,7 +66,7 @@ constexpr int UB = 4;      // transforms per load batch (2*UB loads in flight)
 template <int M, int C>
 __global__ void __launch_bounds__(fft::rows_threads(M), fft::rows_blocks(M)) fwd_rows_kernel(const float* __restrict__ views, int m, int H,
                                                                        int W, int pad, Geo g, int RB,
-                                                                       float2* __restrict__ t1) {
+                                                                       float2* __restrict__ t1, int srgb) {
   SmemPtrs s = carve(g);
   fft::build_tables(g, s.tw1, s.tw2);
   __shared__ int qsrc[MAXQ], qdst[MAXQ];
@@ -95,6 +100,13 @@ __global__ void __launch_bounds__(fft::rows_threads(M), fft::rows_blocks(M)) fwd
           const int o1 = b < B ? qsrc[b] : -1, o2 = b < B ? qsrc[b + B] : -1;
           re[u] = o1 >= 0 ? __ldg(px + o1) : 0.f;
           im[u] = o2 >= 0 ? __ldg(px + o2) : 0.f;
+        }
+        if (srgb) {
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            re[u] = srgb_dec_f(re[u]);
+            im[u] = srgb_dec_f(im[u]);
+          }
         }
 #pragma unroll
         for (int u = 0; u < UB; ++u)
@@ -408,7 +420,7 @@ int persistent_grid(K kernel, int threads, size_t smem, int tiles) {
 
 template <int M>
 int launch_fwd_rows_m(int C, const float* views, int m, int H, int W, int pad, const Geo& g, int RB, float2* t1,
-                      cudaStream_t st) {
+                      int srgb, cudaStream_t st) {
   if (2 * g.B > MAXQ) return fail(FDL_ERR_UNSUPPORTED, "FFT engine: rows tile too large");
   const int threads = round_threads(g);
   const size_t smem = fft::smem_bytes(g);
@@ -416,7 +428,7 @@ int launch_fwd_rows_m(int C, const float* views, int m, int H, int W, int pad, c
 #define FDL_ROWS(CC)                                                                               \
   case CC: {                                                                                       \
     auto k = fwd_rows_kernel<M, CC>;                                                               \
-    k<<<persistent_grid(k, threads, smem, tiles), threads, smem, st>>>(views, m, H, W, pad, g, RB, t1); \
+    k<<<persistent_grid(k, threads, smem, tiles), threads, smem, st>>>(views, m, H, W, pad, g, RB, t1, srgb); \
     break;                                                                                         \
   }
   switch (C) {
@@ -511,7 +523,7 @@ size_t engine_fwd_ws(int m, int H, int W, int C, int pad) {
 }
 
 int engine_fwd(const float* views, int m, int H, int W, int C, int pad, float2* spectra, double* view_sumsq,
-               void* ws, cudaStream_t st) {
+               void* ws, cudaStream_t st, int srgb) {
   const int Hp = H + 2 * pad, Wp = W + 2 * pad, Whp = Wp / 2 + 1;
   Geo gr, gc;
   int RB;
@@ -520,7 +532,7 @@ int engine_fwd(const float* views, int m, int H, int W, int C, int pad, float2* 
   double* partial = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + al256(sizeof(float2) * (size_t)m * C * H * Whp));
   int rc;
   {
-    auto call = [&](auto mm) { return launch_fwd_rows_m<decltype(mm)::value>(C, views, m, H, W, pad, gr, RB, t1, st); };
+    auto call = [&](auto mm) { return launch_fwd_rows_m<decltype(mm)::value>(C, views, m, H, W, pad, gr, RB, t1, srgb, st); };
     switch (gr.M) {
       case 1: rc = call(std::integral_constant<int, 1>()); break;
       case 2: rc = call(std::integral_constant<int, 2>()); break;

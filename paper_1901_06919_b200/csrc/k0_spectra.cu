@@ -18,7 +18,7 @@ namespace fdl {
 bool fft_engine_applies(int Hp, int Wp, int C);
 size_t engine_fwd_ws(int m, int H, int W, int C, int pad);
 int engine_fwd(const float* views, int m, int H, int W, int C, int pad, float2* spectra, double* view_sumsq,
-               void* ws, cudaStream_t st);
+               void* ws, cudaStream_t st, int srgb);
 size_t engine_inv_ws(int V, int C, int Hp, int Wp);
 int engine_inv(const float2* spectra, int V, int C, int Hp, int Wp, int pad, int Ho, int Wo, int srgb, float* images,
                void* ws, cudaStream_t st);
@@ -76,7 +76,7 @@ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // writes one float4 per channel plane (Wp % 4 == 0) or 4 scalars.
 template <int C>
 __global__ void pack_pad_kernel(const float* __restrict__ views, int m, int H, int W, int pad,
-                                float* __restrict__ out) {
+                                float* __restrict__ out, int srgb) {
   const int Hp = H + 2 * pad, Wp = W + 2 * pad;
   const int W4 = (Wp + 3) / 4;
   const size_t total = (size_t)m * Hp * W4;
@@ -95,7 +95,12 @@ __global__ void pack_pad_kernel(const float* __restrict__ views, int m, int H, i
       const bool in = ys >= 0 && ys < H && xs >= 0 && xs < W;
       const float* src = views + (((size_t)j * H + (in ? ys : 0)) * W + (in ? xs : 0)) * C;
 #pragma unroll
-      for (int c = 0; c < C; ++c) v[e][c] = in ? __ldg(src + c) : 0.f;
+      for (int c = 0; c < C; ++c) {
+        float x = in ? __ldg(src + c) : 0.f;
+        // sRGB -> linear light (render.py:39-42), fused into the load
+        if (srgb) x = x <= 0.04045f ? x / 12.92f : powf((fmaxf(x, 0.04045f) + 0.055f) / 1.055f, 2.4f);
+        v[e][c] = x;
+      }
     }
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -112,8 +117,8 @@ __global__ void pack_pad_kernel(const float* __restrict__ views, int m, int H, i
 }
 
 template <int C>
-void launch_pack(const float* views, int m, int H, int W, int pad, float* out, int grid, cudaStream_t st) {
-  pack_pad_kernel<C><<<grid, 256, 0, st>>>(views, m, H, W, pad, out);
+void launch_pack(const float* views, int m, int H, int W, int pad, float* out, int grid, int srgb, cudaStream_t st) {
+  pack_pad_kernel<C><<<grid, 256, 0, st>>>(views, m, H, W, pad, out, srgb);
 }
 
 // sum over (C, Hp, Whp) of |b|^2 per view in float64, deterministic: SPLIT
@@ -240,24 +245,24 @@ int views_to_spectra_ws(int m, int H, int W, int C, int pad, size_t* bytes) {
 }
 
 int views_to_spectra(const float* views, int m, int H, int W, int C, int pad, fdl_c64* spectra,
-                     double* view_sumsq, void* ws, size_t ws_bytes, cudaStream_t st) {
+                     double* view_sumsq, void* ws, size_t ws_bytes, cudaStream_t st, int srgb) {
   const int Hp = H + 2 * pad, Wp = W + 2 * pad, Whp = Wp / 2 + 1;
   size_t need;
   int rc = views_to_spectra_ws(m, H, W, C, pad, &need);
   if (rc) return rc;
   if (ws_bytes < need || (need && !ws)) return fail(FDL_ERR_INVALID, "workspace too small for fdl_views_to_spectra");
   if (fft_engine_applies(Hp, Wp, C))
-    return engine_fwd(views, m, H, W, C, pad, reinterpret_cast<float2*>(spectra), view_sumsq, ws, st);
+    return engine_fwd(views, m, H, W, C, pad, reinterpret_cast<float2*>(spectra), view_sumsq, ws, st, srgb);
   Plan* plan;
   get_plan(Hp, Wp, m * C, 0, &plan);
   float* padded = reinterpret_cast<float*>(ws);
   void* fft_work = reinterpret_cast<char*>(ws) + align256((size_t)m * C * Hp * Wp * sizeof(float));
   const int g = grid_for((size_t)m * Hp * ((Wp + 3) / 4), 256);
   switch (C) {
-    case 1: launch_pack<1>(views, m, H, W, pad, padded, g, st); break;
-    case 2: launch_pack<2>(views, m, H, W, pad, padded, g, st); break;
-    case 3: launch_pack<3>(views, m, H, W, pad, padded, g, st); break;
-    case 4: launch_pack<4>(views, m, H, W, pad, padded, g, st); break;
+    case 1: launch_pack<1>(views, m, H, W, pad, padded, g, srgb, st); break;
+    case 2: launch_pack<2>(views, m, H, W, pad, padded, g, srgb, st); break;
+    case 3: launch_pack<3>(views, m, H, W, pad, padded, g, srgb, st); break;
+    case 4: launch_pack<4>(views, m, H, W, pad, padded, g, srgb, st); break;
     default: return fail(FDL_ERR_UNSUPPORTED, "views support 1..4 channels");
   }
   FDL_LAUNCH_CHECK("pack_pad_kernel");

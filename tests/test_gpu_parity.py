@@ -220,3 +220,40 @@ def test_relaxed_construct_and_render_with_shifts(fdl):
     assert stack.shape == g["stack"].shape
     for j in range(stack.shape[0]):
         assert psnr(stack[j], g["stack"][j]) >= PSNR_MIN
+
+
+def test_srgb_decode_spectra(fdl):
+    # K0 with the fused decode == rfft2 of the padded, decoded views (fp64 numpy)
+    import torch
+    from oracle import fdl_oracle as O
+    from paper_1901_06919_b200 import construct as K
+    rng = np.random.default_rng(5)
+    for (m, h, w, c, pad) in [(3, 40, 52, 3, 6), (2, 64, 64, 1, 12)]:   # cuFFT path and the FFT engine (536-style)
+        imgs = rng.uniform(0, 1, (m, h, w, c)).astype(np.float32)
+        spec, sumsq = K.views_to_spectra(torch.from_numpy(imgs).cuda(), pad, srgb=True)
+        lin = O.srgb_decode(imgs.astype(np.float64))
+        ref, _, _ = O.view_spectra(lin, pad)
+        got = spec.cpu().numpy().reshape(m, c, -1).transpose(2, 0, 1)
+        err = rel_l2(got, ref)
+        print(f"{(m, h, w, c, pad)}: K0 sRGB-decode spectra rel L2 {err:.2e}")
+        assert err < 1e-6
+
+
+@pytest.mark.parametrize("name", ["c1_full"])
+def test_srgb_decode_fused_into_k0(fdl, name):
+    # construct_fdl(decode_srgb=True) == the reference's srgb_decode + construct
+    # (io.py:147-149 then construct.py:219-308), here against the oracle on the
+    # decoded views (the oracle is pinned to the reference by test_oracle.py)
+    from oracle import fdl_oracle as O
+    g = load_golden(name)
+    imgs = np.clip(g["views"], 0.0, 1.0).astype(np.float32)
+    u, v, d = g["u"], g["v"], g["d"]
+    sh = fdl.ShiftParams.factored(u, v, d)
+    model = fdl.construct_fdl(fdl.ViewSet(images=imgs, u=u, v=v), sh, decode_srgb=True)
+    assert model.color_space == fdl.LINEAR
+    ref = O.construct(O.srgb_decode(imgs.astype(np.float64)), np.outer(u, d), np.outer(v, d), d)
+    err = rel_l2(model.layers, ref["layers"])
+    print(f"{name} decode_srgb: layer rel L2 {err:.3e}")
+    assert err <= max(LAYER_TOL, 10 * float(np.max(g["floor"])))
+    with pytest.raises(ValueError):
+        fdl.construct_fdl(fdl.ViewSet(images=imgs, u=u, v=v, color_space=fdl.LINEAR), sh, decode_srgb=True)
