@@ -6,7 +6,9 @@ import sys
 
 rep, units = sys.argv[1], float(sys.argv[2])
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kf = sys.argv[4] if len(sys.argv) > 4 else None  # kernel-name regex for multi-kernel reports
+out = subprocess.run(["ncu", "-i", rep] + (["-k", "regex:" + kf] if kf else []) +
+                     ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout.splitlines()
 agg = collections.defaultdict(lambda: [0.0, 0.0, ""])
 fname = hdr = cur = None
