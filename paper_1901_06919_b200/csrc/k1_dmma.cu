@@ -37,6 +37,12 @@ constexpr int LD = 8;
 #define FDL_K1_KUNROLL 2
 #endif
 constexpr int kKUnroll = FDL_K1_KUNROLL;  // k-step loop unroll (A/B builds)
+#ifndef FDL_K1_TH
+#define FDL_K1_TH 1  // Toeplitz-Hankel Gram from spare RHS columns (0: Gram by DMMA, A/B)
+#endif
+#ifndef FDL_K1_TH_PAIR_MINNB
+#define FDL_K1_TH_PAIR_MINNB 4
+#endif
 #ifndef FDL_K1_PAIR3
 #define FDL_K1_PAIR3 0  // PAIR kernels with NB <= this get 3 CTAs/SM (A/B)
 #endif
@@ -299,7 +305,10 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
   // Toeplitz-Hankel Gram (mode 1, uniform d, off the Nyquist lines, <= 3 channels):
   // G' follows from t[r] = sum_j conj(A_j0) A_jr, which the RHS DMMAs produce for
   // free in the two spare right-hand-side columns (6: Re A_j0, 7: Im A_j0).
-  const bool th = (MODE == MODE_SYMREAL) && p.uniform_d && !nyq_x && !nyq_y && p.C <= 3;
+  // (split systems of <= 2 blocks each -- C2's 15 + 15 -- form the Gram by DMMA instead:
+  //  3 + 3 blocks per k-step are cheaper than the spare-column bookkeeping; measured)
+  const bool th = FDL_K1_TH && (!PAIR || NB > FDL_K1_TH_PAIR_MINNB) && (MODE == MODE_SYMREAL) && p.uniform_d &&
+                  !nyq_x && !nyq_y && p.C <= 3;
 
   // ---------------------------------------------------------------- 1. Gram + RHS
   // mode 1 design matrix (unscaled): M = [Re A_p | -Im A_p | Re A_mid]; the
