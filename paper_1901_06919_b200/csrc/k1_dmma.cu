@@ -44,7 +44,7 @@ constexpr int kKUnroll = FDL_K1_KUNROLL;  // k-step loop unroll (A/B builds)
 #define FDL_K1_TH_PAIR_MINNB 4
 #endif
 #ifndef FDL_K1_PAIR3
-#define FDL_K1_PAIR3 0  // PAIR kernels with NB <= this get 3 CTAs/SM (A/B)
+#define FDL_K1_PAIR3 4  // PAIR kernels with NB <= this get 3 CTAs/SM (80 registers: measured 2 % faster on C2)
 #endif
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -117,6 +117,10 @@ struct FastParams {
 };
 
 __host__ __device__ constexpr int blk(int I, int J) { return I * (I + 1) / 2 + J; }
+// per-warp Toeplitz scratch X (t[] and E of the spare-column Gram): none for the
+// split systems whose Gram the k-steps form by DMMA
+template <int NB, int PAIR>
+__host__ __device__ constexpr int xwords() { return (FDL_K1_TH && (!PAIR || NB > FDL_K1_TH_PAIR_MINNB)) ? NB * 8 * LD : 0; }
 // mode 1 block groups: 0 = cos half (+ the middle column of odd n), 1 = sin half.
 // With mirror pairs (PAIR) blocks of different groups are exactly zero.
 __host__ __device__ constexpr int grp(int I, int NBc) { return (I >= NBc && I < 2 * NBc) ? 1 : 0; }
@@ -184,7 +188,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
   int4* ROW4 = reinterpret_cast<int4*>(PY + py_words);
   YEntry* YT = reinterpret_cast<YEntry*>(PY + py_words);
   const int bs_words = (p.m * p.C + 1) & ~1;  // staged spectra, one float2 per (view, channel); keeps 16-B alignment
-  const int per_warp = px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + NP * LD + bs_words;
+  constexpr int XW = xwords<NB, PAIR>();  // Toeplitz scratch (none when the Gram is formed by DMMA)
+  const int per_warp = px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + XW + bs_words;
   // per column of the real system: (d^4 of its layer(s)) for the lam reg' diagonal
   const int rg_off = py_words + ((ro_words + 1) & ~1);  // 16-byte aligned
   double2* RG = reinterpret_cast<double2*>(smem + rg_off);
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
   double* X = Wst + (NB - 1) * 8 * LD;
   // W = L_KK^-1 of diagonal block K
   auto Wblk = [&](int K) { return K == NB - 1 ? S : Wst + K * 8 * LD; };
-  float2* BS = reinterpret_cast<float2*>(X + NP * LD);
+  float2* BS = reinterpret_cast<float2*>(X + XW);
 
   if (MODE == MODE_SYMREAL) {
     const double2* src = f.py_all + (size_t)i * f.nv * f.hwp;
@@ -716,7 +721,7 @@ int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
   const int ro_words = (MODE == MODE_SYMREAL) ? 2 * ((p.mrow + 3) & ~3) : 3 * p.m * p.n;
   const size_t smem = sizeof(double) * ((size_t)py_words + ro_words + 1 + 2 * NB * 8 +
-                                        (size_t)WARPS * (px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + NB * 8 * LD + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
+                                        (size_t)WARPS * (px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + xwords<NB, PAIR>() + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
   if (smem > 220 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
   auto kern = k1_fast_kernel<NB, MODE, ODD, PAIR>;
   FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
