@@ -7,7 +7,9 @@ import sys
 
 rep = sys.argv[1]
 units = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+kf = sys.argv[4] if len(sys.argv) > 4 else None  # kernel-name regex for multi-kernel reports
+kargs = ["-k", "regex:" + kf] if kf else []
+out = subprocess.run(["ncu", "-i", rep] + kargs + ["--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
 # first kernel section only (a report can list the same launch more than once)
@@ -37,7 +39,7 @@ for r in rows[2:]:
 print(f"warp instructions per unit: {tot / units:.1f}")
 for o, n in op.most_common(int(sys.argv[3]) if len(sys.argv) > 3 else 14):
     print(f"  {o:8s} {n / units:9.1f}  {100 * n / tot:5.1f}%  stall {100 * st[o] / max(totst, 1):5.1f}%")
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
+raw = subprocess.run(["ncu", "-i", rep] + kargs + ["--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
 rr = list(csv.reader(raw))
 keys = ["gpu__time_duration.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "smsp__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
