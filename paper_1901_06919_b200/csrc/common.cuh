@@ -174,5 +174,6 @@ __device__ __forceinline__ void cpa16(void* smem_dst, const void* gsrc, bool val
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cpa_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
 }  // namespace fdl

@@ -200,6 +200,141 @@ __global__ void __launch_bounds__(fft::cols_threads(M), fft::cols_blocks(M)) fwd
   }
 }
 
+// ---------------------------------------------------------------- pipelined column passes
+// Same transforms as fwd_cols_kernel / inv_cols_kernel, but the column tile is
+// brought in by cp.async into the second of two tile buffers while the current
+// tile is transformed, so the global-load latency hides under stage 1 instead
+// of stalling the CTA between its barriers (ncu: long_scoreboard was the top
+// stall of both column kernels).  Zero rows / out-of-range columns use the
+// zero-fill form of the copy.  One thread = (column b, rows ys + t*R), as in
+// the unpipelined kernels; the sum |b|^2 partials keep the same fixed order.
+template <int M>
+__device__ __forceinline__ void cols_issue(const Geo& g, int lb, float2* buf, const float2* __restrict__ src_plane,
+                                           int Whp, int k0, int row_lo, int row_hi, int row_off) {
+  const int B = g.B, b = threadIdx.x & (B - 1), R = blockDim.x >> lb, ys = threadIdx.x >> lb;
+  const bool colok = k0 + b < Whp;
+  // slot n of the transform holds source row n - row_off when row_lo <= n < row_hi
+  for (int n = ys; n < g.N; n += R) {
+    const bool ok = colok && n >= row_lo && n < row_hi;
+    const float2* src = ok ? src_plane + (size_t)(n - row_off) * Whp + k0 + b : src_plane;
+    cpa8(buf + fft::slot_in<M>(g, n) + b, src, ok);
+  }
+  cpa_commit();
+}
+
+template <int M>
+__global__ void __launch_bounds__(fft::cols_threads(M), fft::cols_blocks(M)) fwd_cols_pipe_kernel(
+    const float2* __restrict__ t1, int planes, int H, int pad, int Whp, Geo g, int lb, float2* __restrict__ spec,
+    double* __restrict__ partial) {
+  SmemPtrs s = carve(g);
+  fft::build_tables(g, s.tw1, s.tw2);
+  const int N = g.N, B = g.B, slots = g.slots();
+  const int cblocks = (Whp + B - 1) / B;
+  const int tiles = planes * cblocks;
+  __shared__ double red[32];
+  auto issue = [&](int tile, float2* buf) {
+    const int pl = tile / cblocks, k0 = (tile % cblocks) * B;
+    cols_issue<M>(g, lb, buf, t1 + (size_t)pl * H * Whp, Whp, k0, pad, pad + H, pad);
+  };
+  if ((int)blockIdx.x < tiles) issue(blockIdx.x, s.data);
+  int it = 0;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    float2* cur = s.data + (it & 1) * slots;
+    const int pl = tile / cblocks, k0 = (tile % cblocks) * B;
+    const int b = threadIdx.x & (B - 1), R = blockDim.x >> lb, ys = threadIdx.x >> lb;
+    const bool colok = k0 + b < Whp;
+    __syncthreads();  // the other buffer's previous tile is fully stored
+    if (tile + (int)gridDim.x < tiles) {
+      issue(tile + gridDim.x, s.data + ((it + 1) & 1) * slots);
+      cpa_wait_1();
+    } else {
+      cpa_wait_all();
+    }
+    __syncthreads();
+    fft::stage1<M, false>(g, cur, s.tw1, s.tw2);
+    fft::stage2<M, false>(g, cur);
+    __syncthreads();
+    double acc = 0.0;
+    if (colok) {
+      float2* dst = spec + ((size_t)pl * N + ys) * Whp + k0 + b;
+      const size_t step = (size_t)R * Whp;
+      int k2 = g.divP.div(ys), k1 = ys - k2 * g.P;
+      for (int k = ys; k < N; k += R, dst += step) {
+        const float2 v = cur[k1 * g.SR + k2 * g.SC + b];
+        *dst = v;
+        acc = fma((double)v.x, (double)v.x, acc);
+        acc = fma((double)v.y, (double)v.y, acc);
+        k1 += R;
+        while (k1 >= g.P) {
+          k1 -= g.P;
+          ++k2;
+        }
+      }
+    }
+    if (partial) {
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        partial[tile] = t;
+      }
+    }
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(fft::cols_threads(M), fft::cols_blocks(M)) inv_cols_pipe_kernel(
+    const float2* __restrict__ spec, int planes, int Whp, int pad, int Ho, Geo g, int lb, float2* __restrict__ t2) {
+  SmemPtrs s = carve(g);
+  fft::build_tables(g, s.tw1, s.tw2);
+  const int N = g.N, B = g.B, slots = g.slots();
+  const int cblocks = (Whp + B - 1) / B;
+  const int tiles = planes * cblocks;
+  auto issue = [&](int tile, float2* buf) {
+    const int pl = tile / cblocks, k0 = (tile % cblocks) * B;
+    cols_issue<M>(g, lb, buf, spec + (size_t)pl * N * Whp, Whp, k0, 0, N, 0);
+  };
+  if ((int)blockIdx.x < tiles) issue(blockIdx.x, s.data);
+  int it = 0;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    float2* cur = s.data + (it & 1) * slots;
+    const int pl = tile / cblocks, k0 = (tile % cblocks) * B;
+    const int b = threadIdx.x & (B - 1), R = blockDim.x >> lb, ys = threadIdx.x >> lb;
+    const bool colok = k0 + b < Whp;
+    __syncthreads();
+    if (tile + (int)gridDim.x < tiles) {
+      issue(tile + gridDim.x, s.data + ((it + 1) & 1) * slots);
+      cpa_wait_1();
+    } else {
+      cpa_wait_all();
+    }
+    __syncthreads();
+    fft::stage1<M, true>(g, cur, s.tw1, s.tw2);
+    fft::stage2<M, true>(g, cur);
+    __syncthreads();
+    if (colok) {
+      const size_t step = (size_t)R * Whp;
+      float2* dst = t2 + ((size_t)pl * Ho + ys) * Whp + k0 + b;
+      int k2 = g.divP.div(ys + pad), k1 = ys + pad - k2 * g.P;
+      for (int y = ys; y < Ho; y += R, dst += step) {
+        *dst = cur[k1 * g.SR + k2 * g.SC + b];
+        k1 += R;
+        while (k1 >= g.P) {
+          k1 -= g.P;
+          ++k2;
+        }
+      }
+    }
+  }
+}
+
+inline bool cols_pipe_enabled() {
+  const char* e = getenv("FDL_FFT_PIPE");
+  return e && e[0] == '1';  // opt-in: measured slower (C2b, C4: the second buffer costs a resident CTA)
+}
+
 // per view: sum of its C * cblocks tile partials, fixed order
 __global__ void sumsq_tiles_kernel(const double* __restrict__ partial, int m, int per_view,
                                    double* __restrict__ out) {
@@ -481,6 +616,14 @@ int launch_fwd_cols_m(const float2* t1, int planes, int H, int pad, int Whp, con
   const int threads = round_threads(g);
   const size_t smem = fft::smem_bytes(g);
   const int tiles = planes * ((Whp + g.B - 1) / g.B);
+  const size_t smem2 = smem + sizeof(float2) * (size_t)g.slots();  // second tile buffer
+  if (cols_pipe_enabled() && smem2 <= 227 * 1024) {
+    auto k = fwd_cols_pipe_kernel<M>;
+    k<<<persistent_grid(k, threads, smem2, tiles), threads, smem2, st>>>(t1, planes, H, pad, Whp, g, log2i(g.B),
+                                                                         spec, partial);
+    FDL_LAUNCH_CHECK("fwd_cols_pipe_kernel");
+    return FDL_OK;
+  }
   auto k = fwd_cols_kernel<M>;
   k<<<persistent_grid(k, threads, smem, tiles), threads, smem, st>>>(t1, planes, H, pad, Whp, g, log2i(g.B), spec,
                                                                      partial);
@@ -494,6 +637,14 @@ int launch_inv_cols_m(const float2* spec, int planes, int Whp, int pad, int Ho, 
   const int threads = round_threads(g);
   const size_t smem = fft::smem_bytes(g);
   const int tiles = planes * ((Whp + g.B - 1) / g.B);
+  const size_t smem2 = smem + sizeof(float2) * (size_t)g.slots();
+  if (cols_pipe_enabled() && smem2 <= 227 * 1024) {
+    auto k = inv_cols_pipe_kernel<M>;
+    k<<<persistent_grid(k, threads, smem2, tiles), threads, smem2, st>>>(spec, planes, Whp, pad, Ho, g, log2i(g.B),
+                                                                         t2);
+    FDL_LAUNCH_CHECK("inv_cols_pipe_kernel");
+    return FDL_OK;
+  }
   auto k = inv_cols_kernel<M>;
   k<<<persistent_grid(k, threads, smem, tiles), threads, smem, st>>>(spec, planes, Whp, pad, Ho, g, log2i(g.B), t2);
   FDL_LAUNCH_CHECK("inv_cols_kernel");

@@ -865,20 +865,33 @@ __global__ void __launch_bounds__(128, 4) render_horner2(RenderParams p) {
     }
   }
   if (!inside) return;
-  // out = w_0 * acc, w_0 = exp(2 pi i (pu[v,0] wx + pv[v,0] wy)) from the fp64 tables
+  // out = w_0 * acc, w_0 = exp(2 pi i (pu[v,0] wx + pv[v,0] wy)) from the fp64 tables.
+  // The table loads of a group of EB views are all issued before the group's
+  // stores: p.out may alias p.zx / p.zy as far as the compiler knows, so a
+  // per-view load -> store loop would serialise VB full load latencies.
+  constexpr int EB = (VB + 2) / 3;
 #pragma unroll
-  for (int b = 0; b < VB; ++b) {
-    if (b >= nv) break;
-    const int v = v0 + b;
-    const double2 a = p.zx[((size_t)p.V + v) * p.Whp + kx];
-    const double2 e = p.zy[((size_t)p.V + v) * p.Hp + ky];
-    const u64 w0 = pack2(__double2float_rn(__dsub_rn(__dmul_rn(a.x, e.x), __dmul_rn(a.y, e.y))),
-                         __double2float_rn(__dadd_rn(__dmul_rn(a.x, e.y), __dmul_rn(a.y, e.x))));
+  for (int b0 = 0; b0 < VB; b0 += EB) {
+    double2 a[EB], e[EB];
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      u64 o = 0ull;
-      cmac_w(o, w0, as_f2(acc[b][c]));
-      p.out[((size_t)v * C + c) * Q + q] = as_f2(o);
+    for (int u = 0; u < EB; ++u) {
+      const int v = v0 + min(b0 + u, nv - 1);  // clamped: a valid address, result unused past nv
+      a[u] = p.zx[((size_t)p.V + v) * p.Whp + kx];
+      e[u] = p.zy[((size_t)p.V + v) * p.Hp + ky];
+    }
+#pragma unroll
+    for (int u = 0; u < EB; ++u) {
+      const int b = b0 + u;
+      if (b >= VB || b >= nv) break;
+      const int v = v0 + b;
+      const u64 w0 = pack2(__double2float_rn(__dsub_rn(__dmul_rn(a[u].x, e[u].x), __dmul_rn(a[u].y, e[u].y))),
+                           __double2float_rn(__dadd_rn(__dmul_rn(a[u].x, e[u].y), __dmul_rn(a[u].y, e[u].x))));
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        u64 o = 0ull;
+        cmac_w(o, w0, as_f2(acc[b][c]));
+        p.out[((size_t)v * C + c) * Q + q] = as_f2(o);
+      }
     }
   }
 }
