@@ -159,8 +159,22 @@ __global__ void k1_axis_tables_kernel(SolveParams p, FastParams f) {
   }
 }
 
+// Warps (= bins in flight) per CTA and CTAs per SM.  Mode 2 systems of >= 5
+// blocks (C3: 48 layers, real A) hold the full Gram in registers; at 8 warps x
+// 2 CTAs (128 registers) they spilled 272 B per thread and the spills doubled
+// the kernel's DRAM writes, so they run FDL_K1_REALA_WARPS warps x 2 CTAs.
+#ifndef FDL_K1_REALA_WARPS
+#define FDL_K1_REALA_WARPS 6
+#endif
+template <int NB, int MODE, int PAIR>
+struct K1Cfg {
+  static constexpr int warps = (MODE == MODE_REALA && NB >= 5 && NB <= 6) ? FDL_K1_REALA_WARPS : WARPS;
+  static constexpr int minb = NB <= 2 ? 3 : (PAIR && NB <= FDL_K1_PAIR3 ? 3 : (NB <= 6 ? 2 : 1));
+};
+
 template <int NB, int MODE, int ODD, int PAIR>
-__global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_K1_PAIR3 ? 3 : (NB <= 6 ? 2 : 1)))) k1_fast_kernel(SolveParams p, FastParams f) {
+__global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, MODE, PAIR>::minb) k1_fast_kernel(SolveParams p, FastParams f) {
+  constexpr int WARPS = K1Cfg<NB, MODE, PAIR>::warps;  // shadows the file-wide default
   constexpr int NBc = (NB - ODD) / 2;  // blocks of the cos half (= of the sin half), mode 1
   // blocks I, J interact (PAIR: only within a group)
   auto linked = [](int I, int J) { return !PAIR || grp(I, NBc) == grp(J, NBc); };
@@ -717,6 +731,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NB <= 2 ? 3 : (PAIR && NB <= FDL_
 
 template <int NB, int MODE, int ODD, int PAIR>
 int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
+  constexpr int WARPS = K1Cfg<NB, MODE, PAIR>::warps;
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
   const int ro_words = (MODE == MODE_SYMREAL) ? 2 * ((p.mrow + 3) & ~3) : 3 * p.m * p.n;
