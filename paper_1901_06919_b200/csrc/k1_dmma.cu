@@ -166,10 +166,18 @@ __global__ void k1_axis_tables_kernel(SolveParams p, FastParams f) {
 #ifndef FDL_K1_REALA_WARPS
 #define FDL_K1_REALA_WARPS 6
 #endif
+#ifndef FDL_K1_PAIR_WARPS
+#define FDL_K1_PAIR_WARPS 8  // split (mirror-pair) systems of 3..FDL_K1_PAIR3 blocks (C2)
+#endif
+#ifndef FDL_K1_PAIR_MINB
+#define FDL_K1_PAIR_MINB 3
+#endif
 template <int NB, int MODE, int PAIR>
 struct K1Cfg {
-  static constexpr int warps = (MODE == MODE_REALA && NB >= 5 && NB <= 6) ? FDL_K1_REALA_WARPS : WARPS;
-  static constexpr int minb = NB <= 2 ? 3 : (PAIR && NB <= FDL_K1_PAIR3 ? 3 : (NB <= 6 ? 2 : 1));
+  static constexpr bool pair_small = PAIR && NB > 2 && NB <= FDL_K1_PAIR3;
+  static constexpr int warps =
+      (MODE == MODE_REALA && NB >= 5 && NB <= 6) ? FDL_K1_REALA_WARPS : (pair_small ? FDL_K1_PAIR_WARPS : WARPS);
+  static constexpr int minb = NB <= 2 ? 3 : (pair_small ? FDL_K1_PAIR_MINB : (NB <= 6 ? 2 : 1));
 };
 
 template <int NB, int MODE, int ODD, int PAIR>
