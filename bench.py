@@ -42,14 +42,41 @@ FP64_PEAK_TFLOPS = 36.88  # DMMA m8n8k4 measured on this pool's B200 (profiles/r
 FP32_PEAK_TFLOPS = 73.45  # FFMA2 (fma.rn.f32x2) measured on this pool's B200 (profiles/r01_fp32_pipes.txt)
 
 
-def render_roofline(flops_per_view: float, views: int, k3_s: float, kernel: str) -> dict:
+def render_roofline(flops_per_view: float, views: int, k3_s: float, kernel: str, ktime=None) -> dict:
     """K3 against the FP32 pipe (8C + 6 (+8 with an aperture)
-    flops per (view, bin, layer)); k3_s = K3 seconds (factor pre-pass + tile)."""
-    achieved = flops_per_view * views / k3_s / 1e12 if k3_s > 0 else None
-    return {"bound": "fp32", "kernel": kernel, "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
-            "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS if achieved else None,
-            "flops_per_view": flops_per_view, "k3_ms": 1e3 * k3_s,
-            "peak_source": "measured FFMA2 (tools/microbench/fp32_pipes.cu); MEASURED_PEAKS.json has no fp32 entry"}
+    flops per (view, bin, layer)).  achieved / frac: the step's flops over the
+    main render tile's own launch durations (CUDA events recorded by the library
+    around each launch, `fdl_kernel_timer`); *_stage: over the whole K3 stage
+    k3_s (factor or z pre-pass + tile + Nyquist fix-up + launch gaps)."""
+    ach_stage = flops_per_view * views / k3_s / 1e12 if k3_s > 0 else None
+    out = {"bound": "fp32", "kernel": kernel, "achieved": ach_stage, "peak": FP32_PEAK_TFLOPS,
+           "unit": "TFLOP/s", "frac": ach_stage / FP32_PEAK_TFLOPS if ach_stage else None,
+           "flops_per_view": flops_per_view, "k3_ms": 1e3 * k3_s,
+           "achieved_stage": ach_stage, "frac_stage": ach_stage / FP32_PEAK_TFLOPS if ach_stage else None,
+           "peak_source": "measured FFMA2 (tools/microbench/fp32_pipes.cu); MEASURED_PEAKS.json has no fp32 entry"}
+    if ktime and ktime["s_per_step"] > 0:
+        ach = flops_per_view * views / ktime["s_per_step"] / 1e12
+        out.update({"achieved": ach, "frac": ach / FP32_PEAK_TFLOPS, "kernel_ms_per_launch": ktime["ms_per_launch"],
+                    "launches_per_step": ktime["launches_per_step"]})
+    return out
+
+
+def kernel_timer(on: bool):
+    """Enable (clearing) / disable the library's per-launch events around K1 and K3."""
+    from paper_1901_06919_b200 import _native as nat
+    nat.lib().fdl_kernel_timer(1 if on else 0)
+
+
+def kernel_time(which: int, steps: int):
+    """{s_per_step, ms_per_launch, launches_per_step} of one timed kernel (0: K1, 1: K3), or None."""
+    import ctypes
+    from paper_1901_06919_b200 import _native as nat
+    tot, cnt = ctypes.c_double(0.0), ctypes.c_int32(0)
+    nat.check(nat.lib().fdl_kernel_timer_read(which, ctypes.byref(tot), ctypes.byref(cnt)), "fdl_kernel_timer_read")
+    if cnt.value == 0:
+        return None
+    return {"s_per_step": tot.value / 1e3 / steps, "ms_per_launch": tot.value / cnt.value,
+            "launches_per_step": cnt.value / steps}
 TRAFFIC_FILE = ROOT / "profiles" / "k1_traffic.json"  # dram bytes per K1 launch from `ncu --set full`
 
 
@@ -178,6 +205,7 @@ def run_c5(args, rank, world, device):
     torch.cuda.nvtx.range_push("timed")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     rtim = []
+    kernel_timer(True)
     e0.record(stream)
     for _ in range(args.steps):
         R.render_many_device(model, mine, batch=dev_batch, timing=rtim)
@@ -185,6 +213,8 @@ def run_c5(args, rank, world, device):
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     clocks = sampler.stop()
+    k3_kt = kernel_time(1, args.steps)
+    kernel_timer(False)
     t = e0.elapsed_time(e1) / 1e3 / args.steps
     if world > 1:
         tt = torch.tensor([t], device=device)
@@ -202,7 +232,8 @@ def run_c5(args, rank, world, device):
                        "views_per_step": per_step * world},
             "render_flops_tf": flops_view * per_step / t / 1e12,
             "stages_ms": {"k3_render_spectra_ms": 1e3 * k3_s, "k4_c2r_crop_ms": 1e3 * k4_s},
-            "roofline": render_roofline(flops_view, per_step, k3_s, "K3 render tile (disk aperture, fp32 FFMA2)"),
+            "roofline": render_roofline(flops_view, per_step, k3_s, "K3 render tile (disk aperture, fp32 FFMA2)",
+                                        k3_kt),
             "clocks": clocks, "gpu_launches": args.steps * 4 * math.ceil(per_step / dev_batch)}
 
 
@@ -397,6 +428,7 @@ def run_ours(args, rank, world, device):
     torch.cuda.synchronize()
     sampler = ClockSampler(device.index if device.index is not None else 0)
     sampler.start()
+    kernel_timer(True)
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ isolates the step's launches
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     rtim = []
@@ -413,6 +445,8 @@ def run_ours(args, rank, world, device):
         dist.barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop()
+    k1_kt, k3_kt = kernel_time(0, args.steps), kernel_time(1, args.steps)
+    kernel_timer(False)
     t_con = np.array([e[0].elapsed_time(e[1]) for e in evs]) / 1e3
     t_ren = np.array([e[1].elapsed_time(e[2]) for e in evs]) / 1e3
     t_k1 = np.array([e[3].elapsed_time(e[4]) for e in evs]) / 1e3
@@ -436,7 +470,8 @@ def run_ours(args, rank, world, device):
 
     F_bin = canonical_flops_per_bin(args.config, m, n, C)
     q_k1 = Q_local if sharded else Q  # bins one K1 launch solves on this rank
-    achieved = F_bin * q_k1 / t_k1_mean / 1e12
+    achieved_stage = F_bin * q_k1 / t_k1_mean / 1e12  # over the K1 stage (tables, solve, status count, host sync)
+    achieved = F_bin * q_k1 / k1_kt["s_per_step"] / 1e12 if k1_kt else achieved_stage  # over the solve kernel's launches
     value = Q * n / t_con_mean  # strong scaling: the whole job's bins per max-over-ranks time
     res = {
         "metric": "FDL construction freq·layers/s and rendered views/s",
@@ -461,13 +496,16 @@ def run_ours(args, rank, world, device):
         "render": {"value": V / t_ren_mean, "unit": "views/s", "ms": 1e3 * t_ren_mean,
                    "roofline": render_roofline(Q * n * (8 * C + 6), V // world if world > 1 else V,
                                                stages.get("k3_render_spectra_ms", 0.0) / 1e3,
-                                               "K3 render tile (pinhole, fp32 FFMA2)")},
+                                               "K3 render tile (pinhole, fp32 FFMA2)", k3_kt)},
         "construct_ms": 1e3 * t_con_mean,
         "stages_ms": stages,
         "k1_ms": 1e3 * t_k1_mean,
         "roofline": {"bound": "tensor", "kernel": "k1_fast_kernel (fp64 DMMA)",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS,
+                     "kernel_ms_per_launch": k1_kt["ms_per_launch"] if k1_kt else None,
+                     "launches_per_step": k1_kt["launches_per_step"] if k1_kt else None,
+                     "achieved_stage": achieved_stage, "frac_stage": achieved_stage / FP64_PEAK_TFLOPS,
                      "traffic": k1_traffic(args.config) if world == 1 else None,
                      "algorithmic_bytes": 8 * C * (m + n) * q_k1,
                      "flops_per_bin": F_bin,

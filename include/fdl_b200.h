@@ -77,6 +77,19 @@ const char* fdl_last_error(void);
  * kernels rely on; *max_err receives the largest deviation (synchronises). */
 int fdl_selftest(double* max_err);
 
+/* Kernel-launch timer (measurement instrumentation for bench.py, not part of
+ * the reference interface).  While enabled, the library records a pair of CUDA
+ * events on the launch stream around every launch of its main kernels:
+ *   FDL_TIMER_K1  the per-bin solve kernel of fdl_solve_bins (K1),
+ *   FDL_TIMER_K3  the main render-spectra tile of fdl_render_spectra (K3).
+ * fdl_kernel_timer(1) clears and enables (this host thread); fdl_kernel_timer(0)
+ * disables.  fdl_kernel_timer_read synchronises on the recorded events and
+ * returns the summed launch durations and the launch count of one kernel. */
+#define FDL_TIMER_K1 0
+#define FDL_TIMER_K3 1
+int fdl_kernel_timer(int32_t enable);
+int fdl_kernel_timer_read(int32_t which, double* total_ms, int32_t* launches);
+
 /* ------------------------------------------------------------------------ */
 /* K0: pad + R2C + per-view sum |b|^2   (construct.py:250-266)               */
 /* ------------------------------------------------------------------------ */

@@ -13,6 +13,26 @@
 #include "k3_render.cuh"
 
 namespace fdl {
+struct KTimer {
+  static constexpr int kKinds = 2;
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kKinds];
+};
+static thread_local KTimer t_ktimer;
+
+void ktimer_mark(int which, int phase, cudaStream_t st) {
+  if (!t_ktimer.on || which < 0 || which >= KTimer::kKinds) return;
+  auto& v = t_ktimer.ev[which];
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, st);
+  if (phase == 0) v.emplace_back(e, nullptr);
+  else if (!v.empty() && !v.back().second) v.back().second = e;
+  else cudaEventDestroy(e);
+}
+}  // namespace fdl
+
+namespace fdl {
 
 // --- k0_spectra.cu / k1_*.cu -------------------------------------------------
 int views_to_spectra_ws(int m, int H, int W, int C, int pad, size_t* bytes);
@@ -667,6 +687,34 @@ using namespace fdl;
 extern "C" {
 
 int fdl_version(void) { return 100; }
+
+int fdl_kernel_timer(int32_t enable) {
+  for (auto& v : t_ktimer.ev)
+    for (auto& e : v) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  for (auto& v : t_ktimer.ev) v.clear();
+  t_ktimer.on = enable != 0;
+  return FDL_OK;
+}
+
+int fdl_kernel_timer_read(int32_t which, double* total_ms, int32_t* launches) {
+  if (which < 0 || which >= KTimer::kKinds || !total_ms || !launches) return fail(FDL_ERR_INVALID, "timer kind");
+  double tot = 0.0;
+  int cnt = 0;
+  for (auto& e : t_ktimer.ev[which]) {
+    if (!e.second) continue;  // launch bracket left open (failed launch)
+    FDL_CUDA_CHECK(cudaEventSynchronize(e.second));
+    float ms = 0.f;
+    FDL_CUDA_CHECK(cudaEventElapsedTime(&ms, e.first, e.second));
+    tot += ms;
+    ++cnt;
+  }
+  *total_ms = tot;
+  *launches = cnt;
+  return FDL_OK;
+}
 
 int fdl_selftest(double* max_err) {
   double e = 0;

@@ -176,4 +176,7 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cpa_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
+// kernel-launch timer (abi.cu: fdl_kernel_timer); phase 0 before, 1 after a launch
+void ktimer_mark(int which, int phase, cudaStream_t st);
+
 }  // namespace fdl

@@ -750,7 +750,9 @@ int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
   FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (p.reps < 1) return fail(FDL_ERR_INVALID, "K1 fast path: reps < 1");
   dim3 grid((unsigned)((p.Whp + WARPS * p.reps - 1) / (WARPS * p.reps)), (unsigned)p.nrows);
+  ktimer_mark(0, 0, st);
   kern<<<grid, WARPS * 32, smem, st>>>(p, f);
+  ktimer_mark(0, 1, st);
   FDL_LAUNCH_CHECK("k1_fast_kernel");
   return FDL_OK;
 }

@@ -211,7 +211,9 @@ int k1_generic_launch(const SolveParams& p, cudaStream_t st) {
   const long long nbins = (long long)p.nrows * p.Whp;
   const long long blocks = (nbins + warps - 1) / warps;
   if (blocks == 0) return FDL_OK;
+  ktimer_mark(0, 0, st);
   k1_generic_kernel<<<(unsigned)blocks, warps * 32, smem, st>>>(p);
+  ktimer_mark(0, 1, st);
   FDL_LAUNCH_CHECK("k1_generic_kernel");
   return FDL_OK;
 }

@@ -1288,12 +1288,16 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
   // channels and wins (C2: 0.92 vs 1.08 ms).  FDL_RENDER_KERNEL=horner|fast|legacy overrides.
   const char* rk = getenv("FDL_RENDER_KERNEL");
   if (use_horner2(p)) {
+    ktimer_mark(1, 0, st);
     int rc = launch_horner2<C>(p, st);
+    ktimer_mark(1, 1, st);
     if (rc) return rc;
     return launch_nyquist_fix(p, st);
   }
   if (use_ap_horner(p)) {
+    ktimer_mark(1, 0, st);
     int rc = launch_ap_horner<C>(p, st);
+    ktimer_mark(1, 1, st);
     if (rc) return rc;
     return launch_nyquist_fix(p, st);
   }
@@ -1306,10 +1310,12 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
     const bool ap = p.view_ap != nullptr;
     const int VB = ap ? FastVB<C>::ap : FastVB<C>::pin;
     dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((p.Whp + FX_T - 1) / FX_T), (unsigned)((p.Hp + FY_T - 1) / FY_T));
+    ktimer_mark(1, 0, st);
     if (ap)
       render_ap_fast<C, FastVB<C>::ap><<<grid, 256, 0, st>>>(p);
     else
       render_pin_fast<C, FastVB<C>::pin><<<grid, 256, 0, st>>>(p);
+    ktimer_mark(1, 1, st);
     FDL_LAUNCH_CHECK("render_fast_kernel");
     return FDL_OK;
   }
@@ -1318,6 +1324,7 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
   // view blocks vary fastest: the CTAs that share a layer tile run together and
   // re-read it from L2 instead of HBM (C4/C5 layers are GBs)
   dim3 grid((unsigned)((p.V + VB - 1) / VB), (unsigned)((p.Whp + TX - 1) / TX), (unsigned)((p.Hp + TY - 1) / TY));
+  ktimer_mark(1, 0, st);
   if (p.view_ap && VB == 16 && render_vb_env(true) == 8) {
     dim3 g8((unsigned)((p.V + 7) / 8), grid.y, grid.z);
     launch_ap<C, 8>(p, g8, block, st);
@@ -1328,6 +1335,7 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
     render_pin_kernel<C, 8><<<g8, block, 0, st>>>(p);
   } else
     render_pin_kernel<C, VB><<<grid, block, 0, st>>>(p);
+  ktimer_mark(1, 1, st);
   FDL_LAUNCH_CHECK("render_tile_kernel");
   return FDL_OK;
 }
