@@ -82,18 +82,31 @@ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // Host-side image of a parameter block; offsets are relative to the device base.
 struct Blob {
   std::vector<char> bytes;
+  // dry: only the layout is computed (offsets and size, no payload) -- the
+  // path / workspace queries, which would otherwise build every table too
+  bool dry = false;
+  size_t dry_end = 0;
+  size_t end() const { return dry ? dry_end : bytes.size(); }
   size_t add(const void* src, size_t n) {
-    size_t off = align256(bytes.size());
+    size_t off = align256(end());
+    if (dry) {
+      dry_end = off + n;
+      return off;
+    }
     bytes.resize(off + n);
     if (n) std::memcpy(bytes.data() + off, src, n);
     return off;
   }
   size_t reserve(size_t n) {
-    size_t off = align256(bytes.size());
+    size_t off = align256(end());
+    if (dry) {
+      dry_end = off + n;
+      return off;
+    }
     bytes.resize(off + n);
     return off;
   }
-  size_t size() const { return align256(bytes.size()); }
+  size_t size() const { return align256(end()); }
 };
 
 // Pinned staging ring: the H2D copy of a parameter block must not read
@@ -312,9 +325,14 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
     if (ap.rows < 2 || ap.cols < 2 || !ap.table_re) return fail(FDL_ERR_INVALID, "aperture table needs >= 2x2 entries");
     P.o_tab_re.push_back(B.add(ap.table_re, sizeof(double) * ap.rows * ap.cols));
     P.o_tab_im.push_back(ap.table_im ? B.add(ap.table_im, sizeof(double) * ap.rows * ap.cols) : (size_t)-1);
-    if (!ap.table_im && mode == MODE_REALA) {
+    if (!ap.table_im && mode == MODE_REALA && B.dry) {
+      P.o_quad.push_back(B.reserve(sizeof(double) * 4 * ((size_t)ap.rows * ap.cols + 1)));
+    } else if (!ap.table_im && mode == MODE_REALA) {
+      // built in place in the parameter block (zero-initialised: the last
+      // entry, where out-of-range lookups point, stays 0)
       const size_t R = ap.rows, Cc = ap.cols;
-      std::vector<double> quad(4 * (R * Cc + 1), 0.0);
+      const size_t off = B.reserve(sizeof(double) * 4 * (R * Cc + 1));
+      double* quad = reinterpret_cast<double*>(B.bytes.data() + off);
       for (size_t iy = 0; iy + 1 < R; ++iy)
         for (size_t ix = 0; ix + 1 < Cc; ++ix) {
           double* e = &quad[4 * (iy * Cc + ix)];
@@ -323,7 +341,7 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
           e[2] = ap.table_re[(iy + 1) * Cc + ix];
           e[3] = ap.table_re[(iy + 1) * Cc + ix + 1];
         }
-      P.o_quad.push_back(B.add(quad.data(), quad.size() * sizeof(double)));
+      P.o_quad.push_back(off);
     } else {
       P.o_quad.push_back((size_t)-1);
     }
@@ -541,10 +559,10 @@ int plan_render(const fdl_render_desc* D, RenderPlan& P) {
           e[3] = (float)T[(iy + 1) * Cc + ix + 1];
         }
     };
-    build(ap.table_re);
+    if (!B.dry) build(ap.table_re);
     P.o_re.push_back(B.add(quad.data(), quad.size() * sizeof(float)));
     if (ap.table_im) {
-      build(ap.table_im);
+      if (!B.dry) build(ap.table_im);
       P.o_im.push_back(B.add(quad.data(), quad.size() * sizeof(float)));
     } else {
       P.o_im.push_back((size_t)-1);
@@ -565,7 +583,7 @@ int plan_render(const fdl_render_desc* D, RenderPlan& P) {
       }
       if (total + 2 < (size_t)(INT32_MAX / 2)) {
         std::vector<float4> dq(total + 2, make_float4(0.f, 0.f, 0.f, 0.f));
-        for (int a = 0; a < nap; ++a) {
+        for (int a = 0; a < nap && !B.dry; ++a) {
           const fdl_aperture& ap = D->apertures[a];
           const size_t R = ap.rows, Cc = ap.cols;
           const double* T = ap.table_re;
@@ -759,6 +777,7 @@ int fdl_gather_rows(const fdl_c64* src_dev, int32_t m, int32_t C, int32_t Hp, in
 
 size_t fdl_solve_bins_workspace(const fdl_solve_desc* desc) {
   SolvePlan P;
+  P.blob.dry = true;
   int mode;
   if (plan_solve(desc, P, &mode)) return 0;
   return P.ws_bytes();
@@ -766,6 +785,7 @@ size_t fdl_solve_bins_workspace(const fdl_solve_desc* desc) {
 
 int fdl_solve_path(const fdl_solve_desc* desc) {
   SolvePlan P;
+  P.blob.dry = true;
   int mode;
   int rc = plan_solve(desc, P, &mode);
   return rc ? rc : mode;
@@ -1090,6 +1110,7 @@ int fdl_symmetrize(fdl_c64* layers_dev, int32_t n, int32_t C, int32_t Hp, int32_
 
 size_t fdl_render_workspace(const fdl_render_desc* desc) {
   RenderPlan P;
+  P.blob.dry = true;
   if (plan_render(desc, P)) return 0;
   return render_ws_bytes(P);
 }
