@@ -399,11 +399,13 @@ def run_ours(args, rank, world, device):
         spectra, sumsq = K.views_to_spectra(views, pad)
         if ev is not None:
             ev[2].record(stream)  # K0 done (pack + cuFFT R2C + sum|b|^2)
-        lam = K.lambda_from_sumsq(sumsq.cpu().numpy(), Q, m)
         if ev is not None:
             ev[0].record(stream)
-        layers, nbad, path = K.solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, lam, K.DEFAULT_EPS,
-                                          views=vs_meta, u=None if wide else u, v=None if wide else v)
+        # default lambda read from K0's sums once the solve call is prepared
+        # (construct_fdl's device path does the same)
+        layers, nbad, path = K.solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, None, K.DEFAULT_EPS,
+                                          views=vs_meta, u=None if wide else u, v=None if wide else v,
+                                          lam_fn=lambda: K.lambda_from_sumsq(sumsq.cpu().numpy(), Q, m))
         if ev is not None:
             ev[1].record(stream)
         K.symmetrize(layers, Hp, Wp)

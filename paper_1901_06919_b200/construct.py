@@ -218,13 +218,15 @@ def aperture_table_set(apertures):
 
 
 def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps, views=None,
-               u=None, v=None, force_path=0, status=None, out=None, full_grid=False, count=True):
+               u=None, v=None, force_path=0, status=None, out=None, full_grid=False, count=True, lam_fn=None):
     """Run K1 on a slab of frequency rows; returns (layers (n,C,nrows,Whp) c64, n_breakdown, path).
 
     full_grid: spectra / out are full (.., Hp, Whp) buffers and only `rows` are
     solved, in place (plane_rows = Hp).  count=False skips the breakdown count
     (no host synchronisation; n_breakdown is returned as None and the caller
-    inspects `status`)."""
+    inspects `status`).  lam_fn: lam is None and lam_fn() gives it; it is called
+    only after the descriptor, plan queries and workspace are ready, so the
+    host work of this call overlaps the device work lam_fn waits for (K0)."""
     import torch
     device = spectra.device
     whp = Wp // 2 + 1
@@ -260,7 +262,7 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
         desc.s, desc.scale = nat.dptr(s_), nat.dptr(sc_)
         desc.n_apertures = len(uniq)
         desc.apertures = arr
-    desc.lam, desc.eps = float(lam), float(eps)
+    desc.lam, desc.eps = (float(lam) if lam is not None else 0.0), float(eps)  # lam does not shape the plan
     desc.spectra_dev = spectra.data_ptr()
     desc.layers_dev = layers.data_ptr()
     desc.status_dev = status.data_ptr()
@@ -275,6 +277,9 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
         nat.check(L.fdl_solve_path(desc), "fdl_solve_bins_workspace")
     ws = nat.workspace(ws_bytes, device)
     nb = nat.ctypes.c_int32(0)
+    if lam_fn is not None:
+        lam = float(lam_fn())
+        desc.lam = lam
     nat.check(L.fdl_solve_bins(desc, ws.data_ptr(), ws.numel(), nat.ctypes.byref(nb) if count else None,
                                nat.stream_handle(device)), "fdl_solve_bins")
     if not count:
@@ -437,25 +442,40 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
         spectra, sumsq = views_to_spectra(_views_device(views.images, dev), pad_margin, srgb=decode_srgb)
     else:
         spectra, sumsq = views_to_spectra_host(views.images, pad_margin, dev, srgb=decode_srgb)
-    if lam is None:
+    if eager_host is None:
+        eager_host = not (_is_torch(views.images) and views.images.is_cuda)
+    pipelined = eager_host and Hp >= 4 * PIPELINE_SLABS
+    lam_box = {}
+    lam_fn = None
+    if lam is None and not pipelined:
+        # default lambda needs K0's sums on the host: read them only once the
+        # solve call is prepared (solve_slab), so that host work overlaps K0
+        def lam_fn():
+            lam_box["lam"] = lambda_from_sumsq(sumsq.cpu().numpy(), grid.num_entries, m)
+            return lam_box["lam"]
+    elif lam is None:
         lam = lambda_from_sumsq(sumsq.cpu().numpy(), grid.num_entries, m)
-    if lam < 0:
+    if lam is not None and lam < 0:
         raise ValueError("lam must be non-negative")
     u = views_u = None
     if shifts.is_factored:
         u, views_u = shifts.u, shifts.v
-    if eager_host is None:
-        eager_host = not (_is_torch(views.images) and views.images.is_cuda)
     host = None
-    if eager_host and Hp >= 4 * PIPELINE_SLABS:
+    if pipelined:
         layers, host, path = _solve_pipelined(spectra, m, n, C, Hp, Wp, pu, pv, d, lam, eps, views, u, views_u,
                                               force_path)
         n_bad = 0
         if host is None:  # some bin broke down: the plain path below re-solves with the fallback
             layers = None
     if host is None:
-        layers, n_bad, path = solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, lam, eps,
-                                         views=views, u=u, v=views_u, force_path=force_path)
+        if lam is None and lam_fn is None:  # the pipelined path fell back: its default lambda
+            lam = lambda_from_sumsq(sumsq.cpu().numpy(), grid.num_entries, m)
+        layers, n_bad, path = solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d,
+                                         None if lam_fn is not None and lam is None else lam, eps,
+                                         views=views, u=u, v=views_u, force_path=force_path,
+                                         lam_fn=lam_fn if lam is None else None)
+        if lam is None:
+            lam = lam_box["lam"]
     st = last_construct_stats()
     st.path, st.breakdown_bins, st.lam = path, n_bad, float(lam)
     if n_bad:
