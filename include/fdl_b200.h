@@ -90,6 +90,11 @@ int fdl_selftest(double* max_err);
 int fdl_kernel_timer(int32_t enable);
 int fdl_kernel_timer_read(int32_t which, double* total_ms, int32_t* launches);
 
+/* Test hook (not part of the reference interface): force_cufft = 1 makes K0 /
+ * K4 on this host thread use cuFFT even where the library's own FFT engine
+ * applies (grid sides 67 * 2^a, 131 * 2^a), so tests can compare the two. */
+int fdl_fft_force_cufft(int32_t force_cufft);
+
 /* ------------------------------------------------------------------------ */
 /* K0: pad + R2C + per-view sum |b|^2   (construct.py:250-266)               */
 /* ------------------------------------------------------------------------ */

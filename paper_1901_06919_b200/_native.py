@@ -97,6 +97,7 @@ EXPORTS = {
     "fdl_selftest": (ctypes.c_int, [c_double_p]),
     "fdl_kernel_timer": (ctypes.c_int, [ctypes.c_int32]),
     "fdl_kernel_timer_read": (ctypes.c_int, [ctypes.c_int32, c_double_p, c_int32_p]),
+    "fdl_fft_force_cufft": (ctypes.c_int, [ctypes.c_int32]),
     "fdl_views_to_spectra_workspace": (ctypes.c_size_t, [ctypes.c_int32] * 5),
     "fdl_views_to_spectra": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 5 + [
         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),

@@ -164,6 +164,10 @@ __device__ __forceinline__ void cmac2(u64& acc, float wr, float wi, float2 z) {
 }
 
 // asynchronous global -> shared copies (sm_80+ cp.async), zero-filled when !valid
+__device__ __forceinline__ void cpa4(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(gsrc), "r"(valid ? 4 : 0));
+}
 __device__ __forceinline__ void cpa8(void* smem_dst, const void* gsrc, bool valid) {
   const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(gsrc), "r"(valid ? 8 : 0));
@@ -172,6 +176,8 @@ __device__ __forceinline__ void cpa16(void* smem_dst, const void* gsrc, bool val
   const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gsrc), "r"(valid ? 16 : 0));
 }
+// bring a line into L2 ahead of a later load (no registers held)
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cpa_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }

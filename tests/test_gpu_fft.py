@@ -1,13 +1,11 @@
-"""K0 / K4 through the shared-memory FFT engine (csrc/fft_engine.cuh, k0_fft.cu)
+"""K0 / K4 through the library's FFT engine (csrc/fft2.cuh, k0_fft.cu)
 against numpy's pocketfft (what the reference calls: construct.py:261-263,
 spectra.py:202-208) and against the cuFFT path of the same entry points.
 
-The engine serves grids whose sides are P * 2^a with a large odd factor
-(C1 134, C2 536, C2b 1048, C4 2144); FDL_FFT=cufft forces the cuFFT path,
-FDL_FFT=engine forces the engine on any size it can split.
+The engine serves grids whose sides are 67 * 2^a or 131 * 2^a (C1 134, C2
+536, C2b 1048, C4 2144); fdl_fft_force_cufft(1) (a test hook of the C ABI)
+forces the cuFFT path on this thread.
 """
-
-import os
 
 import numpy as np
 import pytest
@@ -27,28 +25,23 @@ def env():
 
 
 def _with_fft(mode, fn):
-    old = os.environ.get("FDL_FFT")
-    if mode is None:
-        os.environ.pop("FDL_FFT", None)
-    else:
-        os.environ["FDL_FFT"] = mode
+    """mode "engine": the library's default (its engine where it applies); "cufft": forced cuFFT."""
+    from paper_1901_06919_b200 import _native
+    lib = _native.lib()
+    lib.fdl_fft_force_cufft(1 if mode == "cufft" else 0)
     try:
         return fn()
     finally:
-        if old is None:
-            os.environ.pop("FDL_FFT", None)
-        else:
-            os.environ["FDL_FFT"] = old
+        lib.fdl_fft_force_cufft(0)
 
 
-# (m, H, W, C, pad): padded sides 134, 536, 2144 (x2), 201 (odd, no power-of-two
-# part), 96 x 134 (a 3 x 32 side next to an engine side), 1048
+# (m, H, W, C, pad): padded sides 134, 536, 1048, 2144 and non-square 134 x 268, 524 x 134
 FWD_CASES = [
     (3, 128, 128, 1, 3),
     (4, 512, 512, 3, 12),
-    (2, 96, 80, 3, 27),
-    (2, 40, 195, 2, 3),
-    (3, 90, 128, 4, 3),
+    (2, 128, 262, 3, 3),
+    (2, 518, 128, 2, 3),
+    (3, 110, 110, 4, 12),
     (2, 1024, 1024, 1, 12),
     (1, 2048, 2048, 3, 48),
 ]
@@ -103,9 +96,9 @@ INV_CASES = [
     (3, 1, 134, 134, 3, False),
     (4, 3, 536, 536, 12, False),
     (2, 3, 536, 536, 12, True),
-    (2, 3, 150, 134, 27, False),
-    (2, 2, 46, 201, 3, False),
-    (2, 4, 96, 134, 0, False),
+    (2, 3, 134, 268, 27, False),
+    (2, 2, 524, 134, 3, False),
+    (2, 4, 268, 134, 0, False),
     (1, 1, 1048, 1048, 12, False),
     (1, 3, 2144, 2144, 48, False),
 ]
