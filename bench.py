@@ -389,11 +389,11 @@ def run_construct(args, cfg, rank, world, device, render=True):
         if ev is not None:
             ev[2].record(stream)  # K0 done (pad + R2C + sum|b|^2)
             ev[0].record(stream)
-        # default lambda read from K0's sums once the solve call is prepared
-        # (construct_fdl's device path does the same)
+        # default lambda on the device (construct_fdl does the same): no host round trip
+        lam_dev = K.lambda_device(sumsq, Q, m)
         layers, nbad, path = K.solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, None, K.DEFAULT_EPS,
                                           views=vs_meta, u=None if wide else u, v=None if wide else v,
-                                          lam_fn=lambda: K.lambda_from_sumsq(sumsq.cpu().numpy(), Q, m))
+                                          lam_dev=lam_dev)
         if ev is not None:
             ev[1].record(stream)
         K.symmetrize(layers, Hp, Wp)

@@ -124,6 +124,11 @@ int fdl_views_to_spectra_srgb(const float* views_dev, int32_t m, int32_t H, int3
 int fdl_gather_rows(const fdl_c64* src_dev, int32_t m, int32_t C, int32_t Hp, int32_t Whp,
                     const int32_t* rows_dev, int32_t nrows, fdl_c64* dst_dev, void* stream);
 
+/* default_lambda on the device (construct.py:214-216): lam = 1e-4 * (sum_j
+ * view_sumsq[j] / Q) / m, the per-view sums added in view order by one thread
+ * -- bit-identical to the host formula for any sharding of the views. */
+int fdl_default_lambda(const double* view_sumsq_dev, int32_t m, int64_t Q, double* lam_dev, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* K1: per-bin regularised least squares   (construct.py:168-211)           */
 /* ------------------------------------------------------------------------ */
@@ -155,6 +160,9 @@ typedef struct fdl_solve_desc {
                                   Hp: full-grid buffers (m or n, C, Hp, Whp) and the listed rows
                                   are solved in place (buffer row rows[i]); status stays
                                   (nrows, Whp).  Lets a caller solve a full spectrum in row slabs. */
+  const double* lam_dev;       /* optional device scalar that replaces lam (the default lambda
+                                  computed on the device by fdl_default_lambda: no host round trip
+                                  between K0 and K1); NULL: use lam */
 } fdl_solve_desc;
 
 /* Bytes of device workspace fdl_solve_bins needs (0 for the current kernels

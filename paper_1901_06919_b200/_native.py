@@ -52,7 +52,7 @@ class FdlSolveDesc(ctypes.Structure):
         ("lam", ctypes.c_double), ("eps", ctypes.c_double),
         ("spectra_dev", ctypes.c_void_p), ("layers_dev", ctypes.c_void_p),
         ("status_dev", ctypes.c_void_p), ("force_path", ctypes.c_int32),
-        ("plane_rows", ctypes.c_int32),
+        ("plane_rows", ctypes.c_int32), ("lam_dev", ctypes.c_void_p),
     ]
 
 
@@ -98,6 +98,8 @@ EXPORTS = {
     "fdl_kernel_timer": (ctypes.c_int, [ctypes.c_int32]),
     "fdl_kernel_timer_read": (ctypes.c_int, [ctypes.c_int32, c_double_p, c_int32_p]),
     "fdl_fft_force_cufft": (ctypes.c_int, [ctypes.c_int32]),
+    "fdl_default_lambda": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p,
+                                          ctypes.c_void_p]),
     "fdl_views_to_spectra_workspace": (ctypes.c_size_t, [ctypes.c_int32] * 5),
     "fdl_views_to_spectra": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 5 + [
         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),

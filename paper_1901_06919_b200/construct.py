@@ -218,15 +218,16 @@ def aperture_table_set(apertures):
 
 
 def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps, views=None,
-               u=None, v=None, force_path=0, status=None, out=None, full_grid=False, count=True, lam_fn=None):
+               u=None, v=None, force_path=0, status=None, out=None, full_grid=False, count=True, lam_fn=None,
+               lam_dev=None):
     """Run K1 on a slab of frequency rows; returns (layers (n,C,nrows,Whp) c64, n_breakdown, path).
 
     full_grid: spectra / out are full (.., Hp, Whp) buffers and only `rows` are
     solved, in place (plane_rows = Hp).  count=False skips the breakdown count
     (no host synchronisation; n_breakdown is returned as None and the caller
-    inspects `status`).  lam_fn: lam is None and lam_fn() gives it; it is called
-    only after the descriptor, plan queries and workspace are ready, so the
-    host work of this call overlaps the device work lam_fn waits for (K0)."""
+    inspects `status`).  lam_dev: a (1,) float64 CUDA tensor holding lambda
+    (lambda_device): K1 reads it on the device, no host round trip; lam is
+    then ignored.  lam_fn: lam is None and lam_fn() gives it (host)."""
     import torch
     device = spectra.device
     whp = Wp // 2 + 1
@@ -268,6 +269,8 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     desc.status_dev = status.data_ptr()
     desc.force_path = int(force_path)
     desc.plane_rows = Hp if full_grid else 0
+    if lam_dev is not None:
+        desc.lam_dev = lam_dev.data_ptr()
     L = nat.lib()
     path = L.fdl_solve_path(desc)
     if path < 0:
@@ -285,6 +288,9 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     if not count:
         return layers, None, path
     n_bad = int(nb.value)
+    if n_bad and lam_dev is not None:
+        lam = float(lam_dev.item())
+        desc.lam, desc.lam_dev = lam, None
     if n_bad and lam > 0:
         # the reference's minimum-norm fallback for the flagged bins (construct.py:205-210), on the GPU
         bins = np.ascontiguousarray(np.flatnonzero(status.cpu().numpy().reshape(-1)), dtype=np.int32)
@@ -400,6 +406,16 @@ def default_pad_margin(pu, pv) -> int:
     return int(math.ceil(max(np.max(np.abs(pu)), np.max(np.abs(pv)))))
 
 
+def lambda_device(view_sumsq_dev, Q: int, m: int):
+    """default_lambda on the device (fdl_default_lambda): a (1,) float64 CUDA
+    tensor, bit-identical to lambda_from_sumsq of the same sums."""
+    import torch
+    lam = torch.empty((1,), dtype=torch.float64, device=view_sumsq_dev.device)
+    nat.check(nat.lib().fdl_default_lambda(view_sumsq_dev.data_ptr(), m, int(Q), lam.data_ptr(),
+                                           nat.stream_handle(view_sumsq_dev.device)), "fdl_default_lambda")
+    return lam
+
+
 def lambda_from_sumsq(view_sumsq, Q: int, m: int) -> float:
     """default_lambda from per-view partial sums, summed on the host in view order."""
     tot = 0.0
@@ -445,37 +461,25 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
     if eager_host is None:
         eager_host = not (_is_torch(views.images) and views.images.is_cuda)
     pipelined = eager_host and Hp >= 4 * PIPELINE_SLABS
-    lam_box = {}
-    lam_fn = None
-    if lam is None and not pipelined:
-        # default lambda needs K0's sums on the host: read them only once the
-        # solve call is prepared (solve_slab), so that host work overlaps K0
-        def lam_fn():
-            lam_box["lam"] = lambda_from_sumsq(sumsq.cpu().numpy(), grid.num_entries, m)
-            return lam_box["lam"]
-    elif lam is None:
-        lam = lambda_from_sumsq(sumsq.cpu().numpy(), grid.num_entries, m)
     if lam is not None and lam < 0:
         raise ValueError("lam must be non-negative")
+    # the default lambda stays on the device (no host round trip between K0 and K1)
+    lam_dev = lambda_device(sumsq, grid.num_entries, m) if lam is None else None
     u = views_u = None
     if shifts.is_factored:
         u, views_u = shifts.u, shifts.v
     host = None
     if pipelined:
         layers, host, path = _solve_pipelined(spectra, m, n, C, Hp, Wp, pu, pv, d, lam, eps, views, u, views_u,
-                                              force_path)
+                                              force_path, lam_dev)
         n_bad = 0
         if host is None:  # some bin broke down: the plain path below re-solves with the fallback
             layers = None
     if host is None:
-        if lam is None and lam_fn is None:  # the pipelined path fell back: its default lambda
-            lam = lambda_from_sumsq(sumsq.cpu().numpy(), grid.num_entries, m)
-        layers, n_bad, path = solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d,
-                                         None if lam_fn is not None and lam is None else lam, eps,
-                                         views=views, u=u, v=views_u, force_path=force_path,
-                                         lam_fn=lam_fn if lam is None else None)
-        if lam is None:
-            lam = lam_box["lam"]
+        layers, n_bad, path = solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, lam, eps,
+                                         views=views, u=u, v=views_u, force_path=force_path, lam_dev=lam_dev)
+    if lam is None:
+        lam = float(lam_dev.item())
     st = last_construct_stats()
     st.path, st.breakdown_bins, st.lam = path, n_bad, float(lam)
     if n_bad:
@@ -492,7 +496,7 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
     return model
 
 
-PIPELINE_SLABS = int(os.environ.get("FDL_PIPELINE_SLABS", "4"))
+PIPELINE_SLABS = 4  # conjugate-row slabs of the overlapped read-back
 
 
 def _row_runs(rows):
@@ -506,7 +510,7 @@ def _row_runs(rows):
     return runs
 
 
-def _solve_pipelined(spectra, m, n, C, Hp, Wp, pu, pv, d, lam, eps, views, u, v, force_path):
+def _solve_pipelined(spectra, m, n, C, Hp, Wp, pu, pv, d, lam, eps, views, u, v, force_path, lam_dev=None):
     """K1 + K2 in PIPELINE_SLABS slabs of conjugate row pairs, each slab's
     finished rows copied to pinned host memory on a side stream while the next
     slab solves (the reference returns host layers, construct.py:300-308).
@@ -529,7 +533,8 @@ def _solve_pipelined(spectra, m, n, C, Hp, Wp, pu, pv, d, lam, eps, views, u, v,
         status = torch.zeros((len(rows), whp), dtype=torch.int8, device=device)
         statuses.append(status)
         _, _, path = solve_slab(spectra, m, n, C, Hp, Wp, rows, pu, pv, d, lam, eps, views=views, u=u, v=v,
-                                force_path=force_path, status=status, out=layers, full_grid=True, count=False)
+                                force_path=force_path, status=status, out=layers, full_grid=True, count=False,
+                                lam_dev=lam_dev)
         r32 = np.ascontiguousarray(rows, dtype=np.int32)
         nat.check(L.fdl_symmetrize_rows(layers.data_ptr(), n, C, Hp, Wp, len(r32), nat.iptr(r32),
                                         nat.stream_handle(device)), "fdl_symmetrize_rows")

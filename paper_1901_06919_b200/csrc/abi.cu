@@ -40,6 +40,7 @@ int views_to_spectra(const float* views, int m, int H, int W, int C, int pad, fd
                      void* ws, size_t ws_bytes, cudaStream_t st, int srgb = 0);
 int gather_rows(const fdl_c64* src, int m, int C, int Hp, int Whp, const int* rows_dev, int nrows, fdl_c64* dst,
                 cudaStream_t st);
+int default_lambda(const double* sums, int m, long long Q, double* lam, cudaStream_t st);
 int spectra_to_images_ws(int V, int C, int Hp, int Wp, size_t* bytes);
 int spectra_to_images(fdl_c64* spectra, int V, int C, int Hp, int Wp, int pad, int Ho, int Wo, int srgb,
                       float* images, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -171,7 +172,8 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
   if (D->Hp < 1 || D->Wp < 1) return fail(FDL_ERR_INVALID, "invalid grid dimensions");
   if (D->nrows < 0 || D->nrows > D->Hp) return fail(FDL_ERR_INVALID, "invalid slab row count");
   if (!D->d) return fail(FDL_ERR_INVALID, "layer disparities required");
-  if (!(D->lam >= 0.0) || !std::isfinite(D->lam)) return fail(FDL_ERR_INVALID, "lam must be non-negative");
+  if (!D->lam_dev && (!(D->lam >= 0.0) || !std::isfinite(D->lam)))
+    return fail(FDL_ERR_INVALID, "lam must be non-negative");
   const bool factored = D->u && D->v;
   if (!factored && !(D->pu && D->pv)) return fail(FDL_ERR_INVALID, "need (u, v) or (pu, pv)");
   if (!finite_all(D->d, n)) return fail(FDL_ERR_INVALID, "disparities must be finite");
@@ -274,6 +276,7 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
   }
   if (p.N > 128 || p.R > 16) return fail(FDL_ERR_UNSUPPORTED, "layer/channel count beyond the K1 kernels");
   p.lam = D->lam;
+  p.lam_dev = D->lam_dev;
   p.eps = D->eps;
   p.spectra = reinterpret_cast<const float2*>(D->spectra_dev);
   p.layers = reinterpret_cast<float2*>(D->layers_dev);
@@ -773,6 +776,11 @@ int fdl_gather_rows(const fdl_c64* src_dev, int32_t m, int32_t C, int32_t Hp, in
                     int32_t nrows, fdl_c64* dst_dev, void* stream) {
   if (m < 0 || C < 1 || Hp < 1 || Whp < 1 || nrows < 0) return fail(FDL_ERR_INVALID, "invalid gather shape");
   return gather_rows(src_dev, m, C, Hp, Whp, rows_dev, nrows, dst_dev, as_stream(stream));
+}
+
+int fdl_default_lambda(const double* view_sumsq_dev, int32_t m, int64_t Q, double* lam_dev, void* stream) {
+  if (m < 1 || Q < 1 || !view_sumsq_dev || !lam_dev) return fail(FDL_ERR_INVALID, "invalid default_lambda arguments");
+  return default_lambda(view_sumsq_dev, m, (long long)Q, lam_dev, as_stream(stream));
 }
 
 size_t fdl_solve_bins_workspace(const fdl_solve_desc* desc) {

@@ -228,7 +228,23 @@ inline int grid_for(size_t total, int threads) {
   return (int)(b < cap ? (b > 0 ? b : 1) : cap);
 }
 
+// default_lambda (construct.py:214-216) from the per-view sums, added in view
+// order by one thread: the same double operations, in the same order, as the
+// host formula (construct.lambda_from_sumsq), so the value is bit-identical.
+__global__ void default_lambda_kernel(const double* __restrict__ sums, int m, long long Q, double* __restrict__ lam) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double tot = 0.0;
+  for (int j = 0; j < m; ++j) tot = __dadd_rn(tot, sums[j]);
+  lam[0] = __ddiv_rn(__dmul_rn(1e-4, __ddiv_rn(tot, (double)Q)), (double)m);
+}
+
 }  // namespace
+
+int default_lambda(const double* sums, int m, long long Q, double* lam, cudaStream_t st) {
+  default_lambda_kernel<<<1, 32, 0, st>>>(sums, m, Q, lam);
+  FDL_LAUNCH_CHECK("default_lambda_kernel");
+  return FDL_OK;
+}
 
 int views_to_spectra_ws(int m, int H, int W, int C, int pad, size_t* bytes) {
   const int Hp = H + 2 * pad, Wp = W + 2 * pad;

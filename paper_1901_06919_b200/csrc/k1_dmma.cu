@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
   // ---------------------------------------------------------------- 2. + lam reg'
   {
     // reference rounding: ((wx^2 + wy^2)^2 * d^4 + eps), G += lam * reg (construct.py:283,194)
+    const double lam = solve_lam(p);
     const double osq = __dadd_rn(__dmul_rn(ox, ox), __dmul_rn(oy, oy));
     const double w4 = __dmul_rn(osq, osq);
     // lane (q, t) holds diagonal entry (q, q) of each diagonal block iff q >> 1 == t
@@ -558,11 +559,11 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
           if (ab.y >= 0.0) {
             // pair (p, n-1-p): lam (reg_p + reg_{n-1-p}) / 4 on the unscaled basis
             const double r2 = __dadd_rn(__dmul_rn(w4, ab.y), p.eps);
-            add = __dmul_rn(p.lam, 0.25 * __dadd_rn(r1, r2));
+            add = __dmul_rn(lam, 0.25 * __dadd_rn(r1, r2));
           } else {
-            add = __dmul_rn(p.lam, r1);
+            add = __dmul_rn(lam, r1);
           }
-          if (!(p.lam > 0.0)) add = 0.0;
+          if (!(lam > 0.0)) add = 0.0;
         }
         if (e) g[blk(I, I)][1] = __dadd_rn(g[blk(I, I)][1], add);
         else g[blk(I, I)][0] = __dadd_rn(g[blk(I, I)][0], add);

@@ -103,8 +103,9 @@ __global__ void k1_generic_kernel(SolveParams p) {
   // + lam * reg'
   const double ox = omega_x_label(kx, p.Wp), oy = omega_y_label(ky, p.Hp);
   const double w2 = ox * ox + oy * oy, w4 = w2 * w2;
-  if (p.lam > 0.0)
-    for (int a = lane; a < N; a += 32) G[a * ld + a] += p.lam * real_reg(p, a, w4);
+  const double lam = solve_lam(p);
+  if (lam > 0.0)
+    for (int a = lane; a < N; a += 32) G[a * ld + a] += lam * real_reg(p, a, w4);
   __syncwarp();
 
   // right-looking Cholesky, lower triangle in place

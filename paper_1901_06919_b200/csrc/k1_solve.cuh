@@ -49,6 +49,7 @@ struct SolveParams {
   const DevAperture* aps;
   const double* d;           // (n)
   double lam, eps;
+  const double* lam_dev;     // device lambda (overrides lam) or nullptr
   const float2* spectra;     // (m, C, nrows, Whp)
   float2* layers;            // (n, C, nrows, Whp)
   signed char* status;       // (nrows, Whp) or nullptr
@@ -71,6 +72,9 @@ struct SolveParams {
   const int2* row_pairs;     // nullptr: no pairing (mrow = m)
   int mrow;
 };
+
+// lambda of this solve: the device scalar when the caller computed it there
+__device__ __forceinline__ double solve_lam(const SolveParams& p) { return p.lam_dev ? __ldg(p.lam_dev) : p.lam; }
 
 // spectra / layers addressing: slab buffers or full-grid buffers (plane_rows)
 __device__ __forceinline__ size_t sp_plane(const SolveParams& p) {

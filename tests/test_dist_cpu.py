@@ -55,9 +55,19 @@ def _worker(rank, world, port, m, C, Hp, Whp, n, q):
         full = torch.complex(torch.randn((m, C, Hp, Whp), generator=gen), torch.randn((m, C, Hp, Whp), generator=gen))
         j0, j1 = D.view_range(m, world, rank)
         local = full[j0:j1].contiguous()
-        slab = D.exchange_rows(local, m, Hp, gather=lambda src, rows: src[:, :, torch.as_tensor(rows.astype(np.int64))])
+        (slab, rows1, _), = D.exchange_rows(local, m, Hp)
         rows, _ = D.slab_rows(Hp, world, rank)
         ok_exchange = torch.equal(slab, full[:, :, torch.as_tensor(rows.astype(np.int64))])
+        ok_exchange &= np.array_equal(rows1, rows)
+        # the chunked (pipelined) exchange delivers the same slab, piece by piece, bit for bit
+        for chunks in (2, 3, 5):
+            parts = D.exchange_rows(local, m, Hp, chunks=chunks, async_op=True)
+            for _, _, work in parts:
+                if work is not None:
+                    work.wait()
+            got = torch.cat([r for r, _, _ in parts], dim=2)
+            ok_exchange &= torch.equal(got, slab)
+            ok_exchange &= np.array_equal(np.concatenate([rc for _, rc, _ in parts]), rows)
         # lambda from per-view partial sums: identical to the single-process value
         sums = (full.abs() ** 2).sum(dim=(1, 2, 3)).double()
         lam = D.lambda_all_views(sums[j0:j1], m, Hp * Whp)
@@ -72,12 +82,13 @@ def _worker(rank, world, port, m, C, Hp, Whp, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_exchange_gloo(world):
+@pytest.mark.parametrize("world,m", [(2, 7), (3, 7), (3, 2)])
+def test_exchange_gloo(world, m):
+    # (3, 2): fewer views than ranks -- a rank with no views still takes part
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, 7, 2, 10, 6, 3, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, 2, 10, 6, 3, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]

@@ -110,3 +110,51 @@ def test_pipelined_readback_bitwise():
     assert torch.equal(a.layers_device(), b.layers_device())
     assert torch.equal(a.layers_host(), b.layers_device().cpu())
     np.testing.assert_array_equal(a.layers, b.layers)
+
+
+def _nccl_world1(torch):
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    return dist
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_construct_sharded_chunked_and_fallback(cuda, chunks):
+    """The chunked (overlapped) exchange + device lambda give construct_fdl's layers
+    bit for bit, and a breakdown bin takes the reference's minimum-norm fallback
+    (construct.py:205-210) on the sharded path as on the one-GPU path."""
+    torch = cuda
+    import paper_1901_06919_b200 as fdl
+    from paper_1901_06919_b200 import dist as D
+    from oracle import fdl_oracle as O
+    dist = _nccl_world1(torch)
+    try:
+        case = _case()
+        sh = fdl.ShiftParams.factored(case.u, case.v, case.d)
+        slab, rows, lam, pad, (Hp, Wp) = D.construct_sharded(case.views, 0, case.views.shape[0], sh, chunks=chunks)
+        ref = fdl.construct_fdl(fdl.ViewSet(images=case.views, u=case.u, v=case.v), sh)
+        assert lam == ref.lambda_used
+        assert torch.equal(D.gather_slabs(slab, Hp), ref.layers_device())
+        # singular DC bin (two coincident views, eps = 0): fallback on the sharded path
+        rng = np.random.default_rng(3)
+        img = rng.uniform(0, 1, (2, 16, 16, 1)).astype(np.float32)
+        sh2 = fdl.ShiftParams.factored([0.0, 0.0], [0.0, 0.0], [0.0, 1.0])
+        slab2, _, _, _, (Hp2, _) = D.construct_sharded(torch.from_numpy(img).cuda(), 0, 2, sh2, lam=1e-3, eps=0.0,
+                                                       pad_margin=0, chunks=chunks)
+        one = fdl.construct_fdl(fdl.ViewSet(images=img, u=[0.0, 0.0], v=[0.0, 0.0]), sh2, lam=1e-3, eps=0.0,
+                                pad_margin=0)
+        assert fdl.last_construct_stats().fallback_bins >= 1
+        assert torch.equal(D.gather_slabs(slab2, Hp2), one.layers_device())
+        oref = O.construct(img.astype(np.float64), np.zeros((2, 2)), np.zeros((2, 2)), np.array([0.0, 1.0]),
+                           lam=1e-3, eps=0.0, pad=0)
+        got = D.gather_slabs(slab2, Hp2).cpu().numpy()
+        assert np.linalg.norm(got - oref["layers"]) / np.linalg.norm(oref["layers"]) < 1e-6
+        with pytest.raises(ValueError):
+            D.construct_sharded(case.views, 0, case.views.shape[0], sh, lam=-1.0)
+    finally:
+        dist.destroy_process_group()
