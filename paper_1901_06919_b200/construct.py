@@ -38,7 +38,7 @@ __all__ = [
 ]
 
 DEFAULT_EPS = 1e-9       # construct.py:27
-SOLVE_CHUNK = 16384      # construct.py:28 (accepted for API compatibility; K1 has no chunking)
+SOLVE_CHUNK = 16384      # construct.py:28 (K1 solves every bin at once; the chunk is the fallback granularity)
 
 
 class RankDeficiencyError(Exception):
@@ -219,7 +219,7 @@ def aperture_table_set(apertures):
 
 def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps, views=None,
                u=None, v=None, force_path=0, status=None, out=None, full_grid=False, count=True, lam_fn=None,
-               lam_dev=None):
+               lam_dev=None, chunk=None, chunk_sync=None, resolve_only=None):
     """Run K1 on a slab of frequency rows; returns (layers (n,C,nrows,Whp) c64, n_breakdown, path).
 
     full_grid: spectra / out are full (.., Hp, Whp) buffers and only `rows` are
@@ -227,11 +227,16 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     (no host synchronisation; n_breakdown is returned as None and the caller
     inspects `status`).  lam_dev: a (1,) float64 CUDA tensor holding lambda
     (lambda_device): K1 reads it on the device, no host round trip; lam is
-    then ignored.  lam_fn: lam is None and lam_fn() gives it (host)."""
+    then ignored.  lam_fn: lam is None and lam_fn() gives it (host).  chunk:
+    the reference's solve chunk (fallback granularity, fallback_bins).
+    resolve_only: host array of slab bins -- skip K1 and only re-solve those
+    bins by the minimum-norm fallback (lam > 0), into `out`."""
     import torch
     device = spectra.device
     whp = Wp // 2 + 1
     nrows = len(rows)
+    if chunk is None:
+        chunk = SOLVE_CHUNK
     layers = out if out is not None else torch.empty((n, C, Hp if full_grid else nrows, whp),
                                                      dtype=torch.complex64, device=device)
     if status is None:
@@ -275,6 +280,9 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     path = L.fdl_solve_path(desc)
     if path < 0:
         nat.check(path, "fdl_solve_path")
+    if resolve_only is not None:
+        resolve_bins(desc, np.ascontiguousarray(resolve_only, dtype=np.int32), device)
+        return layers, None, path
     ws_bytes = L.fdl_solve_bins_workspace(desc)
     if ws_bytes == 0:
         nat.check(L.fdl_solve_path(desc), "fdl_solve_bins_workspace")
@@ -291,16 +299,46 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     if n_bad and lam_dev is not None:
         lam = float(lam_dev.item())
         desc.lam, desc.lam_dev = lam, None
+    resolved = 0
     if n_bad and lam > 0:
-        # the reference's minimum-norm fallback for the flagged bins (construct.py:205-210), on the GPU
-        bins = np.ascontiguousarray(np.flatnonzero(status.cpu().numpy().reshape(-1)), dtype=np.int32)
-        rws = nat.workspace(L.fdl_resolve_bins_workspace(desc, len(bins)), device)
-        nat.check(L.fdl_resolve_bins(desc, nat.iptr(bins), len(bins), rws.data_ptr(), rws.numel(),
-                                     nat.stream_handle(device)), "fdl_resolve_bins")
+        bins = fallback_bins(status.cpu().numpy().reshape(-1), rows, whp, chunk, chunk_sync)
+        resolve_bins(desc, bins, device)
+        resolved = len(bins)
         n_bad = int(torch.count_nonzero(status).item())
     st = last_construct_stats()
-    st.fallback_bins = int(nb.value) - n_bad
+    st.fallback_bins = resolved - n_bad
     return layers, n_bad, path
+
+
+def fallback_bins(status_flat, rows, whp: int, chunk: int, chunk_sync=None):
+    """Slab bins (row-major flat indices) the reference re-solves by minimum-norm
+    least squares when K1 flagged `status_flat` != 0 (construct.py:196-210):
+    np.linalg.solve raises for the WHOLE chunk of `chunk` consecutive bins
+    (flat q = ky * Whp + kx, construct.py:277-284) that holds a singular normal
+    matrix, and every bin of that chunk is re-solved.  chunk_sync (multi-GPU)
+    merges the bad-chunk sets of all ranks, whose slabs may share a chunk."""
+    rows = np.asarray(rows, dtype=np.int64)
+    bad = np.flatnonzero(status_flat)
+    gq = rows[bad // whp] * whp + bad % whp
+    chunks = np.unique(gq // max(1, int(chunk)))
+    if chunk_sync is not None:
+        chunks = chunk_sync(chunks)
+    allq = (rows[:, None] * whp + np.arange(whp)[None, :]).reshape(-1)
+    return np.ascontiguousarray(np.flatnonzero(np.isin(allq // max(1, int(chunk)), chunks)), dtype=np.int32)
+
+
+RESOLVE_BATCH = 4096  # bins per fdl_resolve_bins call (bounds the workspace: ~m n 16 B per bin)
+
+
+def resolve_bins(desc, bins, device):
+    """The reference's minimum-norm fallback (construct.py:157-165) on the GPU for
+    the listed slab bins, in batches."""
+    L = nat.lib()
+    for b0 in range(0, len(bins), RESOLVE_BATCH):
+        part = np.ascontiguousarray(bins[b0:b0 + RESOLVE_BATCH], dtype=np.int32)
+        rws = nat.workspace(L.fdl_resolve_bins_workspace(desc, len(part)), device)
+        nat.check(L.fdl_resolve_bins(desc, nat.iptr(part), len(part), rws.data_ptr(), rws.numel(),
+                                     nat.stream_handle(device)), "fdl_resolve_bins")
 
 
 def views_to_spectra(views_dev, pad, srgb: bool = False):
@@ -429,9 +467,10 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
                   force_path: int = 0, eager_host: bool | None = None, decode_srgb: bool = False) -> FdlModel:
     """Build the disparity-layer model by per-frequency solves (construct.py:219-308).
 
-    Same arguments, defaults and exceptions as the reference.  `chunk` is
-    accepted and ignored (every bin is solved independently in one launch;
-    results never depend on it).  `device` picks the CUDA device (default:
+    Same arguments, defaults and exceptions as the reference.  Every bin is
+    solved independently in one launch; `chunk` only sets the reference's
+    fallback granularity (a singular bin sends its whole chunk of `chunk`
+    bins to the minimum-norm solve, construct.py:196-210).  `device` picks the CUDA device (default:
     current); `force_path` pins the K1 formulation (testing).  `eager_host`
     (default: when the views came from host memory) reads the layers back to
     pinned host memory slab by slab while later slabs solve; the model's
@@ -443,6 +482,7 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
     if decode_srgb and views.color_space != GAMMA:
         raise ValueError("decode_srgb needs gamma-encoded (sRGB) views")
     torch = _require_cuda()
+    last_construct_stats().fallback_bins = 0
     pu, pv, d = resolve_shifts(views, shifts)
     m = views.num_views
     n = pu.shape[1]
@@ -477,7 +517,8 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
             layers = None
     if host is None:
         layers, n_bad, path = solve_slab(spectra, m, n, C, Hp, Wp, np.arange(Hp), pu, pv, d, lam, eps,
-                                         views=views, u=u, v=views_u, force_path=force_path, lam_dev=lam_dev)
+                                         views=views, u=u, v=views_u, force_path=force_path, lam_dev=lam_dev,
+                                         chunk=chunk)
     if lam is None:
         lam = float(lam_dev.item())
     st = last_construct_stats()

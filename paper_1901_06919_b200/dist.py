@@ -257,22 +257,34 @@ def construct_sharded(views_local, view_offset: int, m: int, shifts, lam=None, e
     if k1_events is not None:
         k1_events[1].record()
     del spectra
-    layers = torch.cat(pieces, dim=2) if len(pieces) != 1 else pieces[0]
     lam_h = float(lam_dev.item()) if lam_dev is not None else float(lam)
-    # breakdown bins: the reference's minimum-norm fallback (construct.py:205-210), like
-    # the one-GPU path (construct.solve_slab), chunk by chunk
-    r0 = 0
-    for recv, rows_c, status in statuses:
-        nb = int(torch.count_nonzero(status).item())
-        if nb:
-            if lam_h == 0:
-                raise RankDeficiencyError("singular normal matrix at some frequency")
-            out = layers[:, :, r0:r0 + len(rows_c)].contiguous()
-            _, left, _ = K.solve_slab(recv, m, n, C, Hp, Wp, rows_c, pu, pv, d, lam_h, eps, views=views_meta, u=u,
-                                      v=v, out=out)
-            if left:
-                raise nat.FdlNativeError(f"{left} bins could not be solved (minimum-norm fallback failed)")
-            layers[:, :, r0:r0 + len(rows_c)] = out
-        r0 += len(rows_c)
+    # breakdown bins: the reference's minimum-norm fallback (construct.py:196-210) at its
+    # granularity -- every bin of a solve chunk that holds a singular bin -- with the
+    # bad-chunk sets of all ranks merged (slabs of different ranks can share a chunk)
+    chunk = K.SOLVE_CHUNK
+    nchunks = -(-Q // chunk)
+    local = np.zeros(nchunks, dtype=np.int32)
+    for (recv, rows_c, status) in statuses:
+        st = status.cpu().numpy().reshape(-1)
+        bad = np.flatnonzero(st)
+        if bad.size:
+            gq = np.asarray(rows_c, dtype=np.int64)[bad // Whp] * Whp + bad % Whp
+            local[np.unique(gq // chunk)] = 1
+    flags = torch.as_tensor(local, device=dev)
+    dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    bad_chunks = np.flatnonzero(flags.cpu().numpy())
+    if bad_chunks.size:
+        if lam_h == 0:
+            raise RankDeficiencyError("singular normal matrix at some frequency")
+        for piece, (recv, rows_c, status) in zip(pieces, statuses):
+            bins = K.fallback_bins(np.zeros(len(rows_c) * Whp, np.int8), rows_c, Whp, chunk,
+                                   chunk_sync=lambda _c: bad_chunks)
+            if bins.size:
+                K.solve_slab(recv, m, n, C, Hp, Wp, rows_c, pu, pv, d, lam_h, eps, views=views_meta, u=u, v=v,
+                             out=piece, status=status, resolve_only=bins)
+                left = int(torch.count_nonzero(status).item())
+                if left:
+                    raise nat.FdlNativeError(f"{left} bins could not be solved (minimum-norm fallback failed)")
+    layers = torch.cat(pieces, dim=2) if len(pieces) != 1 else pieces[0]
     K.symmetrize(layers, Hp, Wp, rows, mirror)
     return layers, rows, lam_h, pad_margin, (Hp, Wp)
