@@ -1301,6 +1301,7 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
     if (rc) return rc;
     return launch_nyquist_fix(p, st);
   }
+  if (p.view_ap && p.fast_ap && !(rk && (rk[0] == 'l' || rk[0] == 'f'))) return render_ap_launch(p, st);
   const bool want_horner = rk && rk[0] == 'h';
   if (p.horner && p.view_ap == nullptr && want_horner) return launch_horner(p, st);
   // aperture batches: the round-1 tile stays the default until the fast

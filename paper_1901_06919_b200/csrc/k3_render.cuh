@@ -57,5 +57,7 @@ struct RenderParams {
 };
 
 int render_launch(const RenderParams& p, cudaStream_t st);
+// real-table aperture batches: the TMA-staged tile (k3_render_ap.cu)
+int render_ap_launch(const RenderParams& p, cudaStream_t st);
 
 }  // namespace fdl
