@@ -51,6 +51,8 @@ extern "C" {
 /* per-bin status written by fdl_solve_bins */
 #define FDL_BIN_OK 0
 #define FDL_BIN_BREAKDOWN 1     /* Cholesky pivot <= 0 or non-finite result */
+#define FDL_BIN_SUSPECT 2       /* solved, but max diag(G) ||x|| / ||rhs|| is large enough that the reference's
+                                   1e-8 residual test (construct.py:198-204) could fire: run fdl_audit_bins */
 
 typedef struct fdl_c64 { float re, im; } fdl_c64;
 
@@ -170,8 +172,9 @@ typedef struct fdl_solve_desc {
 size_t fdl_solve_bins_workspace(const fdl_solve_desc* desc);
 
 /* Solve every bin of the slab.  Returns FDL_OK even when some bins break
- * down; they are flagged in status_dev (and counted in *n_breakdown when
- * non-NULL, which synchronises the stream). */
+ * down or are suspect; they are flagged in status_dev (FDL_BIN_BREAKDOWN /
+ * FDL_BIN_SUSPECT) and counted together in *n_breakdown when non-NULL (which
+ * synchronises the stream). */
 int fdl_solve_bins(const fdl_solve_desc* desc, void* workspace_dev, size_t workspace_bytes,
                    int32_t* n_breakdown, void* stream);
 
@@ -186,6 +189,19 @@ int fdl_solve_path(const fdl_solve_desc* desc);
 size_t fdl_resolve_bins_workspace(const fdl_solve_desc* desc, int32_t nbins);
 int fdl_resolve_bins(const fdl_solve_desc* desc, const int32_t* bins, int32_t nbins, void* workspace_dev,
                      size_t workspace_bytes, void* stream);
+
+/* The reference's per-bin acceptance test (construct.py:198-210) on the bins
+ * fdl_solve_bins marked FDL_BIN_SUSPECT: A, b and reg of each listed bin are
+ * rebuilt on the device, the normal equations are solved in fp64 (LDL^H), and a
+ * bin whose residual ||G x - rhs||_F exceeds 1e-8 ||rhs||_F is re-solved by the
+ * minimum-norm `_stacked_lstsq` (lam > 0).  The layers of every listed bin are
+ * rewritten and status_dev becomes FDL_BIN_OK / FDL_BIN_BREAKDOWN.
+ * audit_status (HOST, nbins; the call synchronises): 0 normal equations
+ * accepted, 2 minimum-norm fallback used, 1 fallback failed, 3 test failed at
+ * lam = 0 (the reference raises RankDeficiencyError).  Workspace: as
+ * fdl_resolve_bins_workspace.  desc->lam_dev must be NULL (pass lam). */
+int fdl_audit_bins(const fdl_solve_desc* desc, const int32_t* bins, int32_t nbins, int8_t* audit_status,
+                   void* workspace_dev, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Explicit per-bin systems   (solve_frequency, construct.py:123-165)        */
@@ -311,6 +327,25 @@ int fdl_spectra_to_images(fdl_c64* spectra_dev, int32_t V, int32_t C, int32_t Hp
                           int32_t Wp, int32_t pad, int32_t Ho, int32_t Wo, int32_t srgb,
                           float* images_dev, void* workspace_dev, size_t workspace_bytes,
                           void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* K6: GPU-resident pipeline report and service quantisation                 */
+/*     (pipeline.py:30-51,205-218; serve.py:127)                             */
+/* ------------------------------------------------------------------------ */
+
+/* sqerr_dev (V, C) float64 <- sum over pixels of (images - ref)^2 per view and
+ * channel, the numerators of `psnr` / `mse_per_channel` (pipeline.py:30-51):
+ * images_dev (V, H, W, C) f32 renders, ref_dev (V, H, W, C) the input views
+ * (f32, or f64 when ref_is_f64 != 0).  Differences and sums in float64, fixed
+ * summation order (the report does not depend on scheduling). */
+size_t fdl_view_sqerr_workspace(int32_t V, int32_t C);
+int fdl_view_sqerr(const float* images_dev, const void* ref_dev, int32_t ref_is_f64, int32_t V, int32_t H,
+                   int32_t W, int32_t C, double* sqerr_dev, void* workspace_dev, size_t workspace_bytes,
+                   void* stream);
+
+/* out_dev[i] = uint8(round_half_even(clip(images_dev[i], 0, 1) * 255)), evaluated
+ * in float64 like the service's encoder input (serve.py:127). */
+int fdl_images_to_u8(const float* images_dev, int64_t count, uint8_t* out_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -17,6 +17,7 @@ import numpy as np
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libfdl_b200.so"
 
 FDL_OK = 0
+FDL_BIN_SUSPECT = 2
 FDL_ERR_INVALID = -1
 FDL_ERR_CUDA = -2
 FDL_ERR_UNSUPPORTED = -3
@@ -114,6 +115,8 @@ EXPORTS = {
     "fdl_resolve_bins_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlSolveDesc), ctypes.c_int32]),
     "fdl_resolve_bins": (ctypes.c_int, [ctypes.POINTER(FdlSolveDesc), c_int32_p, ctypes.c_int32, ctypes.c_void_p,
                                         ctypes.c_size_t, ctypes.c_void_p]),
+    "fdl_audit_bins": (ctypes.c_int, [ctypes.POINTER(FdlSolveDesc), c_int32_p, ctypes.c_int32, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "fdl_solve_dense_workspace": (ctypes.c_size_t, [ctypes.POINTER(FdlDenseDesc)]),
     "fdl_solve_dense": (ctypes.c_int, [ctypes.POINTER(FdlDenseDesc), ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p]),
@@ -133,6 +136,10 @@ EXPORTS = {
     "fdl_render_workspace_bound": (ctypes.c_size_t, [ctypes.c_int32] * 6 + [ctypes.c_int64]),
     "fdl_render_spectra": (ctypes.c_int, [ctypes.POINTER(FdlRenderDesc), ctypes.c_void_p,
                                           ctypes.c_size_t, ctypes.c_void_p]),
+    "fdl_view_sqerr_workspace": (ctypes.c_size_t, [ctypes.c_int32] * 2),
+    "fdl_view_sqerr": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int32] * 5 + [
+        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "fdl_images_to_u8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "fdl_spectra_to_images_workspace": (ctypes.c_size_t, [ctypes.c_int32] * 4),
     "fdl_spectra_to_images": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 8 + [
         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
@@ -207,6 +214,29 @@ def aperture_structs(specs):
                              xi0_x=float(xi_x[0]), step_x=float(xi_x[1] - xi_x[0]),
                              xi0_y=float(xi_y[0]), step_y=float(xi_y[1] - xi_y[0]))
     return arr, keep
+
+
+def on_device(pick):
+    """Decorator: run the call with the CUDA device `pick(*args, **kwargs)` current
+    (None: leave the current device).  The native layer launches on the
+    current device's streams and keeps per-device staging, so every host entry
+    point selects the device of the tensors it is handed first."""
+    import functools
+
+    def deco(fn):
+        @functools.wraps(fn)
+        def call(*args, **kwargs):
+            dev = pick(*args, **kwargs)
+            if dev is None:
+                return fn(*args, **kwargs)
+            import torch
+            dev = torch.device(dev)
+            if dev.type != "cuda":
+                return fn(*args, **kwargs)
+            with torch.cuda.device(dev):
+                return fn(*args, **kwargs)
+        return call
+    return deco
 
 
 def stream_handle(device=None):

@@ -75,6 +75,7 @@ def build_system_row(view: ViewSet, j: int, omega, d, grid: FrequencyGrid | None
     return row
 
 
+@nat.on_device(lambda A, b, reg, lam, device=None: device)
 def solve_dense(A, b, reg, lam: float, device=None):
     """Batched explicit regularised solves on the GPU (fdl_solve_dense).
 
@@ -165,6 +166,7 @@ class ConstructStats:
         self.path = 0              # K1 formulation: 1 symmetric-real, 2 real-A, 3 complex
         self.breakdown_bins = 0    # bins left unsolved
         self.fallback_bins = 0     # bins re-solved by the minimum-norm fallback
+        self.audited_bins = 0      # bins the residual screen sent to the reference's exact test
         self.lam = None
 
 
@@ -217,9 +219,10 @@ def aperture_table_set(apertures):
     return uniq, np.asarray(idx, dtype=np.int32)
 
 
+@nat.on_device(lambda spectra, *a, **k: spectra.device)
 def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps, views=None,
                u=None, v=None, force_path=0, status=None, out=None, full_grid=False, count=True, lam_fn=None,
-               lam_dev=None, chunk=None, chunk_sync=None, resolve_only=None):
+               lam_dev=None, chunk=None, chunk_sync=None, resolve_only=None, audit_only=None):
     """Run K1 on a slab of frequency rows; returns (layers (n,C,nrows,Whp) c64, n_breakdown, path).
 
     full_grid: spectra / out are full (.., Hp, Whp) buffers and only `rows` are
@@ -229,6 +232,8 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     (lambda_device): K1 reads it on the device, no host round trip; lam is
     then ignored.  lam_fn: lam is None and lam_fn() gives it (host).  chunk:
     the reference's solve chunk (fallback granularity, fallback_bins).
+    audit_only: host array of slab bins -- skip K1 and run the reference's residual
+    test on those (returns their verdicts in place of the breakdown count);
     resolve_only: host array of slab bins -- skip K1 and only re-solve those
     bins by the minimum-norm fallback (lam > 0), into `out`."""
     import torch
@@ -283,6 +288,8 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
     if resolve_only is not None:
         resolve_bins(desc, np.ascontiguousarray(resolve_only, dtype=np.int32), device)
         return layers, None, path
+    if audit_only is not None:  # the residual test on FDL_BIN_SUSPECT bins -> their verdicts
+        return layers, audit_bins(desc, np.ascontiguousarray(audit_only, dtype=np.int32), device), path
     ws_bytes = L.fdl_solve_bins_workspace(desc)
     if ws_bytes == 0:
         nat.check(L.fdl_solve_path(desc), "fdl_solve_bins_workspace")
@@ -300,10 +307,23 @@ def solve_slab(spectra, m, n, C, Hp, Wp, rows, shifts_pu, shifts_pv, d, lam, eps
         lam = float(lam_dev.item())
         desc.lam, desc.lam_dev = lam, None
     resolved = 0
+    if n_bad:
+        flags = status.cpu().numpy().reshape(-1)
+        suspects = np.flatnonzero(flags == nat.FDL_BIN_SUSPECT)
+        if suspects.size:
+            # the reference's own residual test (construct.py:198-210) on the bins the screen
+            # marked: accepted bins keep a normal-equation solve, failing bins are re-solved
+            # by minimum-norm least squares one by one (lam = 0: they stay flagged and
+            # construct_fdl raises RankDeficiencyError)
+            verdicts = audit_bins(desc, suspects.astype(np.int32), device)
+            last_construct_stats().audited_bins += int(suspects.size)
+            resolved += int(np.count_nonzero(verdicts == 2))
+            flags = status.cpu().numpy().reshape(-1)
+        n_bad = int(np.count_nonzero(flags))
     if n_bad and lam > 0:
-        bins = fallback_bins(status.cpu().numpy().reshape(-1), rows, whp, chunk, chunk_sync)
+        bins = fallback_bins(flags, rows, whp, chunk, chunk_sync)
         resolve_bins(desc, bins, device)
-        resolved = len(bins)
+        resolved += len(bins)
         n_bad = int(torch.count_nonzero(status).item())
     st = last_construct_stats()
     st.fallback_bins = resolved - n_bad
@@ -330,6 +350,22 @@ def fallback_bins(status_flat, rows, whp: int, chunk: int, chunk_sync=None):
 RESOLVE_BATCH = 4096  # bins per fdl_resolve_bins call (bounds the workspace: ~m n 16 B per bin)
 
 
+def audit_bins(desc, bins, device):
+    """The reference's per-bin acceptance test (construct.py:198-210) on the listed slab
+    bins (fdl_audit_bins), in batches -> int8 verdicts: 0 normal equations accepted,
+    2 minimum-norm fallback used, 1 fallback failed, 3 residual test failed at lam = 0."""
+    L = nat.lib()
+    out = np.zeros(len(bins), dtype=np.int8)
+    for b0 in range(0, len(bins), RESOLVE_BATCH):
+        part = np.ascontiguousarray(bins[b0:b0 + RESOLVE_BATCH], dtype=np.int32)
+        verdict = np.zeros(len(part), dtype=np.int8)
+        rws = nat.workspace(L.fdl_resolve_bins_workspace(desc, len(part)), device)
+        nat.check(L.fdl_audit_bins(desc, nat.iptr(part), len(part), verdict.ctypes.data, rws.data_ptr(), rws.numel(),
+                                   nat.stream_handle(device)), "fdl_audit_bins")
+        out[b0:b0 + len(part)] = verdict
+    return out
+
+
 def resolve_bins(desc, bins, device):
     """The reference's minimum-norm fallback (construct.py:157-165) on the GPU for
     the listed slab bins, in batches."""
@@ -341,6 +377,7 @@ def resolve_bins(desc, bins, device):
                                      nat.stream_handle(device)), "fdl_resolve_bins")
 
 
+@nat.on_device(lambda views_dev, *a, **k: views_dev.device)
 def views_to_spectra(views_dev, pad, srgb: bool = False):
     """K0 on a (m,H,W,C) float32 CUDA tensor -> (spectra (m,C,Hp,Whp) c64, per-view sum|b|^2 (m) f64).
     srgb: the views are sRGB-encoded and are decoded to linear light as K0 loads them."""
@@ -364,6 +401,7 @@ def views_to_spectra(views_dev, pad, srgb: bool = False):
 UPLOAD_CHUNK_BYTES = 24 << 20
 
 
+@nat.on_device(lambda images, pad, device, *a, **k: device)
 def views_to_spectra_host(images, pad, device, chunk_bytes: int = UPLOAD_CHUNK_BYTES, srgb: bool = False):
     """K0 on HOST views with the upload overlapped: view chunks go host->device
     on a side stream while K0 transforms the previous chunk on the current
@@ -416,6 +454,7 @@ def views_to_spectra_host(images, pad, device, chunk_bytes: int = UPLOAD_CHUNK_B
     return spectra, sumsq
 
 
+@nat.on_device(lambda layers, *a, **k: layers.device)
 def symmetrize(layers, Hp, Wp, rows=None, mirror=None):
     n, C, nrows, _ = layers.shape
     L = nat.lib()
@@ -462,6 +501,7 @@ def lambda_from_sumsq(view_sumsq, Q: int, m: int) -> float:
     return 1e-4 * (tot / Q) / m
 
 
+@nat.on_device(lambda views, shifts, *a, device=None, **k: device)
 def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None, eps: float = DEFAULT_EPS,
                   pad_margin: int | None = None, chunk: int = SOLVE_CHUNK, *, device=None,
                   force_path: int = 0, eager_host: bool | None = None, decode_srgb: bool = False) -> FdlModel:
@@ -483,6 +523,7 @@ def construct_fdl(views: ViewSet, shifts: ShiftParams, lam: float | None = None,
         raise ValueError("decode_srgb needs gamma-encoded (sRGB) views")
     torch = _require_cuda()
     last_construct_stats().fallback_bins = 0
+    last_construct_stats().audited_bins = 0
     pu, pv, d = resolve_shifts(views, shifts)
     m = views.num_views
     n = pu.shape[1]
@@ -551,6 +592,7 @@ def _row_runs(rows):
     return runs
 
 
+@nat.on_device(lambda spectra, *a, **k: spectra.device)
 def _solve_pipelined(spectra, m, n, C, Hp, Wp, pu, pv, d, lam, eps, views, u, v, force_path, lam_dev=None):
     """K1 + K2 in PIPELINE_SLABS slabs of conjugate row pairs, each slab's
     finished rows copied to pinned host memory on a side stream while the next

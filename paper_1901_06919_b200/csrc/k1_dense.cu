@@ -368,7 +368,8 @@ __global__ void scatter_bins_kernel(SolveParams p, const int* bins, int nb, cons
     const double2 v = x[(size_t)t * p.n * p.C + e];
     p.layers[((size_t)k * p.C + c) * plane + sp_boff(p, i, kx)] = make_float2((float)v.x, (float)v.y);
   }
-  if (threadIdx.x == 0 && p.status) p.status[bin] = st[t] == 2 ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
+  // 0: normal equations accepted, 2: minimum-norm solution; 1 / 3: failed / singular at lam = 0
+  if (threadIdx.x == 0 && p.status) p.status[bin] = (st[t] == 2 || st[t] == 0) ? FDL_BIN_OK : FDL_BIN_BREAKDOWN;
 }
 
 }  // namespace

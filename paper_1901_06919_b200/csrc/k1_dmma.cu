@@ -571,6 +571,25 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
     }
   }
 
+  // screen inputs of the reference's residual test (abi.cu: k1_screen_kernel):
+  // ||rhs||_F^2 over the 2C right-hand sides and the largest diagonal entry of G
+  if (p.audit) {
+    double rs = 0.0, dm = 0.0;
+    const bool dl = (q >> 1) == t;
+#pragma unroll
+    for (int I = 0; I < NB; ++I) {
+      if (2 * t < 2 * p.C) rs = fma(r[I][0], r[I][0], rs);
+      if (2 * t + 1 < 2 * p.C) rs = fma(r[I][1], r[I][1], rs);
+      if (dl && RG[I * 8 + q].x >= 0.0) dm = fmax(dm, (q & 1) ? g[blk(I, I)][1] : g[blk(I, I)][0]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      rs += __shfl_xor_sync(FULL, rs, o);
+      dm = fmax(dm, __shfl_xor_sync(FULL, dm, o));
+    }
+    if (lane == 0) p.audit[soff] = make_double2(rs, dm);
+  }
+
   // ---------------------------------------------------------------- 3. Cholesky + forward
   // Steps of one diagonal block, or (PAIR) of two -- cos block s and sin block
   // NBc + s, factored side by side by lanes 0..7 and 8..15 -- then the middle

@@ -108,6 +108,17 @@ __global__ void k1_generic_kernel(SolveParams p) {
     for (int a = lane; a < N; a += 32) G[a * ld + a] += lam * real_reg(p, a, w4);
   __syncwarp();
 
+  if (p.audit) {  // screen inputs of the residual test: ||rhs||_F^2 and max diag(G)
+    double rs = 0.0, dm = 0.0;
+    for (int e = lane; e < N * R; e += 32) rs = fma(Rh[e], Rh[e], rs);
+    for (int a = lane; a < N; a += 32) dm = fmax(dm, G[a * ld + a]);
+    for (int o = 16; o > 0; o >>= 1) {
+      rs += __shfl_xor_sync(0xffffffffu, rs, o);
+      dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    }
+    if (lane == 0) p.audit[bin] = make_double2(rs, dm);
+  }
+
   // right-looking Cholesky, lower triangle in place
   bool ok = true;
   for (int k = 0; k < N; ++k) {

@@ -264,8 +264,15 @@ def construct_sharded(views_local, view_offset: int, m: int, shifts, lam=None, e
     chunk = K.SOLVE_CHUNK
     nchunks = -(-Q // chunk)
     local = np.zeros(nchunks, dtype=np.int32)
-    for (recv, rows_c, status) in statuses:
+    audited = 0
+    for piece, (recv, rows_c, status) in zip(pieces, statuses):
         st = status.cpu().numpy().reshape(-1)
+        suspects = np.flatnonzero(st == nat.FDL_BIN_SUSPECT)
+        if suspects.size:  # the residual test itself, exactly as the 1-GPU path runs it
+            _, verdicts, _ = K.solve_slab(recv, m, n, C, Hp, Wp, rows_c, pu, pv, d, lam_h, eps, views=views_meta,
+                                          u=u, v=v, out=piece, status=status, audit_only=suspects)
+            audited += int(np.count_nonzero(verdicts == 2))
+            st = status.cpu().numpy().reshape(-1)
         bad = np.flatnonzero(st)
         if bad.size:
             gq = np.asarray(rows_c, dtype=np.int64)[bad // Whp] * Whp + bad % Whp

@@ -184,6 +184,7 @@ def _uses_aperture(req: RenderRequest) -> bool:
     return req.f > 0 and req.aperture is not None and not req.aperture.is_pinhole
 
 
+@nat.on_device(lambda layers_dev, *a, **k: layers_dev.device)
 def render_spectra_batch(layers_dev, d, Hp, Wp, pu, pv, t=None, view_ap=None, apertures=(), oob=None,
                          start_event=None):
     """K3 over V views -> (V, C, Hp, Whp) complex64 CUDA tensor."""
@@ -225,6 +226,7 @@ def render_spectra_batch(layers_dev, d, Hp, Wp, pu, pv, t=None, view_ap=None, ap
     return out
 
 
+@nat.on_device(lambda spec, *a, **k: spec.device)
 def spectra_to_images(spec, Hp, Wp, pad, Ho, Wo, srgb=False):
     """K4: (V, C, Hp, Whp) complex64 (destroyed) -> (V, Ho, Wo, C) float32 CUDA tensor."""
     import torch
@@ -247,6 +249,7 @@ def _check_gamma(model: FdlModel, req: RenderRequest):
                          f"(model stores {model.color_space!r} data)")
 
 
+@nat.on_device(lambda model, *a, **k: model.device)
 def render_many_device(model: FdlModel, reqs, batch: int = 64, timing=None, on_batch=None):
     """Render requests to a (V, H, W, C) float32 CUDA tensor (cropped per req.crop,
     which must agree across the batch) plus per-view OOB counts.  Device-resident
@@ -410,6 +413,12 @@ def render(model: FdlModel, req: RenderRequest) -> np.ndarray:
 
 def render_views_with_shifts(model: FdlModel, shifts) -> np.ndarray:
     """Pinhole views with explicit per-(view, layer) shifts (render.py:251-263): (m, H, W[, C])."""
+    return _to_numpy_images(render_shifts_device(model, shifts))
+
+
+@nat.on_device(lambda model, *a, **k: model.device)
+def render_shifts_device(model: FdlModel, shifts):
+    """`render_views_with_shifts` without the read-back: (m, H, W, C) float32 CUDA tensor."""
     pu, pv = shifts.expand()
     layers = model.layers_device()
     Hp, Wp = model.grid.height, model.grid.width
@@ -417,5 +426,4 @@ def render_views_with_shifts(model: FdlModel, shifts) -> np.ndarray:
     Ho = model.height if pad else Hp
     Wo = model.width if pad else Wp
     spec = render_spectra_batch(layers, model.disparities, Hp, Wp, np.asarray(pu), np.asarray(pv))
-    imgs = spectra_to_images(spec, Hp, Wp, pad, Ho, Wo)
-    return _to_numpy_images(imgs)
+    return spectra_to_images(spec, Hp, Wp, pad, Ho, Wo)

@@ -157,3 +157,22 @@ def test_reference_residual_fallback_semantics():
             gw = g_weighted_error(out["layers"], g["layers"], g["u"], g["v"], g["d"], float(g["lam"]), hp, wp,
                                   eps=float(g["eps"]))
             assert gw < 1e-10, gw
+
+
+def test_reference_residual_test_fires_without_a_singular_matrix():
+    """"residfire" (tests/golden/make_nearsingular.py): every normal matrix is positive
+    definite, np.linalg.solve does not raise, and the reference's residual test
+    (construct.py:198-204) still re-solves ONE bin (LU residual 1.39e-8).  The oracle
+    flags the same bin and reproduces the reference's layers."""
+    g = load_golden("residfire")
+    assert int(g["flagged"].sum()) == 1 and 1e-8 < np.nanmax(g["lu_residual"]) < 2e-8
+    pu, pv = np.outer(g["u"], g["d"]), np.outer(g["v"], g["d"])
+    out = O.construct(g["views"], pu, pv, g["d"], lam=float(g["lam"]), eps=float(g["eps"]), pad=int(g["pad"]),
+                      return_flags=True)
+    assert out["fallback_bins"] == 1
+    from gweight import g_weighted_error
+    hp = g["views"].shape[1] + 2 * int(g["pad"])
+    wp = g["views"].shape[2] + 2 * int(g["pad"])
+    gw = g_weighted_error(out["layers"], g["layers"], g["u"], g["v"], g["d"], float(g["lam"]), hp, wp,
+                          eps=float(g["eps"]))
+    assert gw < 1e-8, gw
