@@ -517,6 +517,8 @@ extern "C" int fdl_fft_force_cufft(int32_t force_cufft) {
 }
 
 // ------------------------------------------------------------------ entry points used by k0_spectra.cu
+bool fft_cufft_forced() { return t_force_cufft != 0; }
+
 bool fft_engine_applies(int Hp, int Wp, int C) {
   return !t_force_cufft && C >= 1 && C <= 4 && side_supported(Hp) && side_supported(Wp);
 }

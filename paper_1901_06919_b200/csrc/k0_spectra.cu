@@ -16,6 +16,12 @@ namespace fdl {
 
 // k0_fft.cu: the shared-memory FFT engine path
 bool fft_engine_applies(int Hp, int Wp, int C);
+bool fft_cufft_forced();
+// k4_mr.cu: mixed-radix K4 (1920 x 1080 grids)
+bool mr_engine_applies(int Hp, int Wp, int C);
+size_t mr_engine_inv_ws(int V, int C, int Ho, int Wp);
+int mr_engine_inv(const float2* spectra, int V, int C, int Hp, int Wp, int pad, int Ho, int Wo, int srgb, float* images,
+                  void* ws, cudaStream_t st);
 size_t engine_fwd_ws(int m, int H, int W, int C, int pad);
 int engine_fwd(const float* views, int m, int H, int W, int C, int pad, float2* spectra, double* view_sumsq,
                void* ws, cudaStream_t st, int srgb);
@@ -312,6 +318,10 @@ int spectra_to_images_ws(int V, int C, int Hp, int Wp, size_t* bytes) {
     *bytes = engine_inv_ws(V, C, Hp, Wp);
     return FDL_OK;
   }
+  if (mr_engine_applies(Hp, Wp, C) && !fft_cufft_forced()) {
+    *bytes = mr_engine_inv_ws(V, C, Hp, Wp);  // (the crop is not known here: Ho <= Hp)
+    return FDL_OK;
+  }
   Plan* plan;
   int rc = get_plan(Hp, Wp, V * C, 1, &plan);
   if (rc) return rc;
@@ -328,6 +338,8 @@ int spectra_to_images(fdl_c64* spectra, int V, int C, int Hp, int Wp, int pad, i
   if (pad < 0 || Ho + pad > Hp || Wo + pad > Wp) return fail(FDL_ERR_INVALID, "crop window outside the grid");
   if (fft_engine_applies(Hp, Wp, C))
     return engine_inv(reinterpret_cast<const float2*>(spectra), V, C, Hp, Wp, pad, Ho, Wo, srgb, images, ws, st);
+  if (mr_engine_applies(Hp, Wp, C) && !fft_cufft_forced())
+    return mr_engine_inv(reinterpret_cast<const float2*>(spectra), V, C, Hp, Wp, pad, Ho, Wo, srgb, images, ws, st);
   Plan* plan;
   get_plan(Hp, Wp, V * C, 1, &plan);
   float* planes = reinterpret_cast<float*>(ws);

@@ -101,6 +101,12 @@ INV_CASES = [
     (2, 4, 268, 134, 0, False),
     (1, 1, 1048, 1048, 12, False),
     (1, 3, 2144, 2144, 48, False),
+    # mixed-radix engine (csrc/fft_mr.cuh, k4_mr.cu): config 5's 1920 x 1080 grid, both orientations,
+    # odd view / channel counts (ragged tiles), a crop and the sRGB epilogue
+    (2, 3, 1080, 1920, 0, False),
+    (1, 1, 1080, 1920, 0, True),
+    (3, 2, 1920, 1080, 4, False),
+    (1, 4, 1080, 1080, 7, False),
 ]
 
 
