@@ -407,7 +407,7 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
     }
   }
   P.o_cnt = B.reserve(sizeof(unsigned long long));
-  P.audit_bytes = sizeof(double2) * (size_t)D->nrows * (size_t)(D->Wp / 2 + 1);
+  P.audit_bytes = sizeof(float2) * (size_t)D->nrows * (size_t)(D->Wp / 2 + 1);
   if (factored) {
     // distinct u and v values -> per-axis phase tables (A_jk = px(u_j) py(v_j), construct.py:174)
     auto distinct = [](const double* x, int m, std::vector<double>& vals, std::vector<int>& idx) {
@@ -488,7 +488,7 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
 
 void bind_solve(SolvePlan& P, const fdl_solve_desc* D, void* ws) {
   SolveParams& p = P.p;
-  p.audit = D->status_dev ? reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + P.blob.size() + align256(P.extra))
+  p.audit = D->status_dev ? reinterpret_cast<float2*>(reinterpret_cast<char*>(ws) + P.blob.size() + align256(P.extra))
                           : nullptr;
   p.rows = at<int>(ws, P.o_rows);
   p.pu = at<double>(ws, P.o_pu);
@@ -556,8 +556,8 @@ __global__ void k1_screen_kernel(SolveParams p) {
       xs1 = fmaf(v.y, v.y, xs1);
     }
     const double xs = (double)xs0 + (double)xs1;
-    const double2 a = p.audit[bin];  // (||rhs||^2, max diag G)
-    const bool suspect = a.x > 0.0 ? a.y * a.y * xs > SCREEN_RHO * SCREEN_RHO * a.x : xs > 0.0;
+    const float2 a = p.audit[bin];  // (||rhs||^2, max diag G)
+    const bool suspect = a.x > 0.f ? (double)a.y * (double)a.y * xs > SCREEN_RHO * SCREEN_RHO * (double)a.x : xs > 0.0;
     if (suspect) p.status[bin] = FDL_BIN_SUSPECT;
   }
 }

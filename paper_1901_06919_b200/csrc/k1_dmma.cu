@@ -582,12 +582,13 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
       if (2 * t + 1 < 2 * p.C) rs = fma(r[I][1], r[I][1], rs);
       if (dl && RG[I * 8 + q].x >= 0.0) dm = fmax(dm, (q & 1) ? g[blk(I, I)][1] : g[blk(I, I)][0]);
     }
+    float rsf = (float)rs, dmf = (float)dm;  // a screen with a 10x margin: fp32 reductions
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      rs += __shfl_xor_sync(FULL, rs, o);
-      dm = fmax(dm, __shfl_xor_sync(FULL, dm, o));
+      rsf += __shfl_xor_sync(FULL, rsf, o);
+      dmf = fmaxf(dmf, __shfl_xor_sync(FULL, dmf, o));
     }
-    if (lane == 0) p.audit[soff] = make_double2(rs, dm);
+    if (lane == 0) p.audit[soff] = make_float2(rsf, dmf);
   }
 
   // ---------------------------------------------------------------- 3. Cholesky + forward

@@ -116,7 +116,7 @@ __global__ void k1_generic_kernel(SolveParams p) {
       rs += __shfl_xor_sync(0xffffffffu, rs, o);
       dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
     }
-    if (lane == 0) p.audit[bin] = make_double2(rs, dm);
+    if (lane == 0) p.audit[bin] = make_float2((float)rs, (float)dm);
   }
 
   // right-looking Cholesky, lower triangle in place

@@ -53,7 +53,7 @@ struct SolveParams {
   const float2* spectra;     // (m, C, nrows, Whp)
   float2* layers;            // (n, C, nrows, Whp)
   signed char* status;       // (nrows, Whp) or nullptr
-  double2* audit;            // (nrows, Whp) per-bin (||rhs||_F^2, max diag G) for the residual screen, or nullptr
+  float2* audit;             // (nrows, Whp) per-bin (||rhs||_F^2, max diag G) for the residual screen, or nullptr
   int uniform_d;             // d_k = d_0 + k delta (Toeplitz Gram available)
   int uniform_ap;            // >= 0: every view uses aperture uniform_ap (mode 2 hoists its fields)
   int reps;                  // K1 fast path: bins per warp (CTAs cover reps * 8 columns)
