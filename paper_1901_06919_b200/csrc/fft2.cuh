@@ -62,7 +62,11 @@ struct Plan {
   static constexpr int SMEM = TABLE_BYTES + TEAMS * TEAM_BYTES;
   // column passes: a group of QT teams moves GC adjacent columns together, so
   // every row segment a warp loads or stores is GC * 8 contiguous bytes
-  static constexpr int GC = T >= 4 ? T : 4;              // columns per group
+#ifndef FDL_FFT_GC
+#define FDL_FFT_GC 8
+#endif
+  static constexpr int GC0 = T >= FDL_FFT_GC ? T : FDL_FFT_GC;  // columns per group: 64-byte row segments
+  static constexpr int GC = GC0 / T <= TEAMS ? GC0 : T * TEAMS; // (at most the CTA's teams)
   static constexpr int QT = GC / T;                      // teams per group
   static constexpr int GROUPS = TEAMS / QT;
   static constexpr int GL = QT * TL;                     // lanes per group

@@ -76,7 +76,14 @@ __global__ void __launch_bounds__(PL::THREADS, 1) fwd_rows_kernel(const float* _
   const int tw = gridDim.x * PL::TEAMS;
   // load mapping: lane = (t, n2, g) as in stage 1; rows n1 = g, g + LV, ...
   const int lg = lane >> 5, lt = (lane & 31) / M, ln2 = lane % M;  // warp lg loads rows n1 = lg (mod LV)
-  for (int item = gw; item < items; item += tw) {
+  // The teams of a CTA take consecutive transforms (= the channels of the same
+  // image rows) and start every round together: their loads of the shared
+  // interleaved sectors then reach L2 within microseconds of each other (at
+  // TB/s an L2 line lives ~40 us; unsynchronised teams re-read the views 2.3x).
+  for (int base = blockIdx.x * PL::TEAMS; base < items; base += tw) {
+    __syncthreads();
+    const int item = base + (gw - blockIdx.x * PL::TEAMS);
+    if (item >= items) continue;
     {
       const int tr = item * T + lt;
       const bool ok = tr < ntr;
@@ -344,7 +351,12 @@ __global__ void __launch_bounds__(PL::THREADS, 1) inv_rows_kernel(const float2* 
   // team index, made visibly warp-uniform (lets stage 1 use the uniform datapath)
   const int gw = __shfl_sync(0xffffffffu, blockIdx.x * PL::TEAMS + (threadIdx.x >> 5) / PL::TEAM_WARPS, 0);
   const int tw = gridDim.x * PL::TEAMS;
-  for (int item = gw; item < items; item += tw) {
+  // rounds start together (see fwd_rows_kernel): the teams' channel-interleaved
+  // stores to the same sectors then merge in L2
+  for (int base = blockIdx.x * PL::TEAMS; base < items; base += tw) {
+    __syncthreads();
+    const int item = base + (gw - blockIdx.x * PL::TEAMS);
+    if (item >= items) continue;
     // Hermitian completion: Z[k] = X[k] + i Y[k], Z[N-k] = conj X[k] + i conj Y[k]
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
