@@ -361,7 +361,6 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
   {
     const long long ctas = (long long)D->nrows * ((p.Whp + 7) / 8);
     p.reps = ctas >= 148LL * 2 * 16 ? 4 : 1;
-    if (const char* e = getenv("FDL_K1_REPS")) p.reps = std::max(1, atoi(e));
   }
 
   Blob& B = P.blob;
@@ -439,8 +438,7 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
     P.has_axes = true;
     // mirror pairs (k1_solve.cuh): every view paired with its (-u, -v) twin or at the origin
     p.mrow = m;
-    const char* pe = getenv("FDL_K1_PAIR");
-    if (mode == MODE_SYMREAL && D->force_path != 5 && !(pe && pe[0] == '0')) {
+    if (mode == MODE_SYMREAL && D->force_path != 5) {
       std::vector<int> partner(m, -2);
       bool all = true;
       for (int j = 0; j < m && all; ++j) {

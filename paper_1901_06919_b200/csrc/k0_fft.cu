@@ -57,7 +57,6 @@ __device__ inline Smem<PL> carve_and_build() {
   return s;
 }
 
-constexpr int UL = 8;  // loads in flight per lane in the load loops
 
 // ---------------------------------------------------------------- K0 rows
 // transform tr -> (view j, row pair yp, channel c), channels fastest so the
@@ -351,6 +350,8 @@ __global__ void __launch_bounds__(PL::THREADS, 1) inv_rows_kernel(const float2* 
   // team index, made visibly warp-uniform (lets stage 1 use the uniform datapath)
   const int gw = __shfl_sync(0xffffffffu, blockIdx.x * PL::TEAMS + (threadIdx.x >> 5) / PL::TEAM_WARPS, 0);
   const int tw = gridDim.x * PL::TEAMS;
+  // every load of a transform's two input rows in flight at once (<= 18 x 2 float2 per lane)
+  constexpr int ULR = (Whp + PL::TL - 1) / PL::TL < 18 ? (Whp + PL::TL - 1) / PL::TL : 18;
   // rounds start together (see fwd_rows_kernel): the teams' channel-interleaved
   // stores to the same sectors then merge in L2
   for (int base = blockIdx.x * PL::TEAMS; base < items; base += tw) {
@@ -370,16 +371,16 @@ __global__ void __launch_bounds__(PL::THREADS, 1) inv_rows_kernel(const float2* 
       const float2* i1 = i0 + Whp;
       float2* b = s.buf + t * M;
 #pragma unroll 1
-      for (int k0 = lane; k0 < Whp; k0 += PL::TL * UL) {
-        float2 X[UL], Y[UL];
+      for (int k0 = lane; k0 < Whp; k0 += PL::TL * ULR) {
+        float2 X[ULR], Y[ULR];
 #pragma unroll
-        for (int u = 0; u < UL; ++u) {
+        for (int u = 0; u < ULR; ++u) {
           const int k = k0 + PL::TL * u;
           X[u] = (ok && k < Whp) ? __ldg(i0 + k) : make_float2(0.f, 0.f);
           Y[u] = (ok && has1 && k < Whp) ? __ldg(i1 + k) : make_float2(0.f, 0.f);
         }
 #pragma unroll
-        for (int u = 0; u < UL; ++u) {
+        for (int u = 0; u < ULR; ++u) {
           const int k = k0 + PL::TL * u;
           if (k >= Whp) break;
           const bool self = k == 0 || 2 * k == N;  // self-conjugate: keep the real parts only

@@ -51,9 +51,6 @@ struct RenderParams {
   const double* h_beta;    // (V)
   double2* zx;             // (V, Whp)
   double2* zy;             // (V, Hp)
-  // aperture Horner tile: the factor pre-pass writes only the lookup halves,
-  // 8-byte {frac, idx} entries at ((float2*)px)[(v n + k) Whp + kx] (rows likewise)
-  int aux8;
 };
 
 int render_launch(const RenderParams& p, cudaStream_t st);

@@ -195,20 +195,21 @@ def test_render_c5_small_matches_reference(fdl):
         assert p >= PSNR_MIN, (i, p)
 
 
-@pytest.mark.parametrize("tile", ["legacy", "fast", "aph"])
-def test_render_c5_small_every_tile(fdl, monkeypatch, tile):
-    """The aperture render tiles behind FDL_RENDER_KERNEL (round-1 tile, direct
-    fast tile, aperture Horner tile) against the reference's renders."""
-    monkeypatch.setenv("FDL_RENDER_KERNEL", tile)
+def test_render_c5_small_complex_table_uses_generic_tile(fdl):
+    """A complex aperture table takes the generic per-view-table tile (real tables take the
+    TMA-staged tile, covered by test_render_c5_small / test_render_many_matches_single): a
+    table with a zero imaginary part added must render the same views."""
     g = load_golden("render_c5_small")
     n, C, hp, whp = g["layers"].shape
     model = fdl.FdlModel(disparities=g["d"], layers=g["layers"], grid=fdl.FrequencyGrid(40, hp), width=40,
                          height=hp)
     ap = golden_spec(fdl, g)
-    reqs = [fdl.RenderRequest(u=g["u"][i], v=g["v"][i], s=g["s"][i], f=g["f"][i], aperture=ap)
+    apc = fdl.ApertureSpec(shape="golden-complex", pad_factor=4, table=np.asarray(ap.table).astype(np.complex128),
+                           xi_x=ap.xi_x, xi_y=ap.xi_y)
+    reqs = [fdl.RenderRequest(u=g["u"][i], v=g["v"][i], s=g["s"][i], f=g["f"][i], aperture=apc)
             for i in range(len(g["u"]))]
     for i, img in enumerate(fdl.render_many(model, reqs)):
-        assert psnr(img, g["renders"][i]) >= PSNR_MIN, (tile, i)
+        assert psnr(img, g["renders"][i]) >= PSNR_MIN, i
 
 
 def test_render_many_matches_single(fdl):
