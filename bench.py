@@ -310,11 +310,11 @@ def run_c5(args, rank, world, device):
            "views_per_rank": V, "batch": batch,
            "stages_ms": {"k3_render_spectra_ms": 1e3 * k3_s, "k4_c2r_crop_ms": 1e3 * k4_s},
            "roofline": render_roofline(flops_view, V, k3_s, "K3 render tile (disk aperture, fp32 FFMA2)", k3_kt),
-           "k4_roofline": hbm_roofline("K4 inverse FFT + crop (Hermitian fix + cuFFT C2R + crop)", k4_bytes, k4_s,
-                                       "spectra read once (8 C Q B/view) + images written (4 H W C B/view)"),
+           "k4_roofline": hbm_roofline("K4 inverse FFT + crop (mixed-radix engine: column pass + row pass)", k4_bytes,
+                                       k4_s, "spectra read once (8 C Q B/view) + images written (4 H W C B/view)"),
            "clocks": clocks,
-           # per launch set: factor pre-pass + aperture tile + Hermitian fix + C2R + crop
-           "gpu_launches": args.steps * 5 * math.ceil(V / batch)}
+           # per launch set: factor pre-pass + TMA aperture tile + K4 column pass + K4 row pass
+           "gpu_launches": args.steps * 4 * math.ceil(V / batch)}
     return res, model, reqs
 
 
@@ -501,9 +501,10 @@ def run_construct(args, cfg, rank, world, device, render=True):
                      "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r01_fp64_pipes.txt); "
                                     "MEASURED_PEAKS.json has no fp64 entry"},
         "clocks": clocks,
-        # K0 (rows + cols + lambda partials) 3, K1 (axis tables + solve + status count) 3, K2 1; renders:
-        # z tables + tile + Nyquist fix-up + K4 column pass + K4 row pass = 5 per launch set
-        "gpu_launches": args.steps * ((7 + world if sharded else 7)
+        # K0 (rows + cols + per-view sums) 3, default lambda 1, K1 (axis tables + solve + residual screen +
+        # status count) 4, K2 1; renders: z tables + tile + Nyquist fix-up + K4 column pass + K4 row pass = 5
+        # per launch set
+        "gpu_launches": args.steps * ((9 + world if sharded else 9)
                                       + 5 * math.ceil((V // world + 1 if sharded else V) / dev_batch)),
     }
     if not sharded:
