@@ -738,12 +738,20 @@ int launch_sum(const RenderParams& p, cudaStream_t st) {
 
 }  // namespace
 
+int render_factors_kernel_launch(const RenderParams& p, cudaStream_t st) {
+  render_factors_kernel<<<p.V * p.n, 256, 0, st>>>(p);
+  FDL_LAUNCH_CHECK("render_factors_kernel");
+  return FDL_OK;
+}
+
 int render_launch(const RenderParams& p0, cudaStream_t st) {
   if (p0.V == 0) return FDL_OK;
   const RenderParams& p = p0;
-  if (!(p.view_ap == nullptr && p.horner)) {  // the pinhole Horner tile needs no per-layer factors
-    render_factors_kernel<<<p.V * p.n, 256, 0, st>>>(p);
-    FDL_LAUNCH_CHECK("render_factors_kernel");
+  // per-layer factor tables: every tile but the pinhole Horner tile and the affine
+  // aperture tile (k3_render_ap.cu, which runs its own 8-byte lookup pre-pass)
+  const bool own_prepass = p.horner && (p.view_ap == nullptr || p.fast_ap);
+  if (!own_prepass) {
+    if (int rc = render_factors_kernel_launch(p, st)) return rc;
   }
   switch (p.C) {
     case 1: return launch_sum<1>(p, st);

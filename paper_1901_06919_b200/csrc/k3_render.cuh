@@ -56,5 +56,7 @@ struct RenderParams {
 int render_launch(const RenderParams& p, cudaStream_t st);
 // real-table aperture batches: the TMA-staged tile (k3_render_ap.cu)
 int render_ap_launch(const RenderParams& p, cudaStream_t st);
+// the 16-byte per-(view, layer) axis factor pre-pass (k3_render.cu)
+int render_factors_kernel_launch(const RenderParams& p, cudaStream_t st);
 
 }  // namespace fdl
