@@ -68,12 +68,12 @@ def hbm_peak():
         return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback (of fallback)"
 
 
-def hbm_roofline(kernel: str, bytes_per_step: float, s_per_step: float, note: str = "") -> dict:
+def hbm_roofline(kernel: str, bytes_per_step: float, s_per_step: float, note: str = "", traffic=None) -> dict:
     peak, src = hbm_peak()
     ach = bytes_per_step / s_per_step / 1e9 if s_per_step > 0 else None
     out = {"bound": "hbm", "kernel": kernel, "achieved": ach, "peak": peak, "unit": "GB/s",
            "frac": ach / peak if ach else None, "algorithmic_bytes": bytes_per_step, "ms": 1e3 * s_per_step,
-           "peak_source": src}
+           "traffic": traffic, "peak_source": src}
     if note:
         out["note"] = note
     return out
@@ -309,9 +309,12 @@ def run_c5(args, rank, world, device):
     res = {"value": len(reqs) / t, "unit": "views/s", "ms": 1e3 * t, "views_per_step": len(reqs),
            "views_per_rank": V, "batch": batch,
            "stages_ms": {"k3_render_spectra_ms": 1e3 * k3_s, "k4_c2r_crop_ms": 1e3 * k4_s},
-           "roofline": render_roofline(flops_view, V, k3_s, "K3 render tile (disk aperture, fp32 FFMA2)", k3_kt),
+           "roofline": {**render_roofline(flops_view, V, k3_s, "K3 render tile (disk aperture, fp32 FFMA2)", k3_kt),
+                        "traffic": k1_traffic("k3_c5") if batch == C5_BATCH else None},
            "k4_roofline": hbm_roofline("K4 inverse FFT + crop (mixed-radix engine: column pass + row pass)", k4_bytes,
-                                       k4_s, "spectra read once (8 C Q B/view) + images written (4 H W C B/view)"),
+                                       k4_s, "spectra read once (8 C Q B/view) + images written (4 H W C B/view); "
+                                       "traffic: ncu DRAM bytes per 256-view launch",
+                                       traffic=k1_traffic("k4_c5") if batch == C5_BATCH else None),
            "clocks": clocks,
            # per launch set: factor pre-pass + TMA aperture tile + K4 column pass + K4 row pass
            "gpu_launches": args.steps * 4 * math.ceil(V / batch)}
@@ -511,7 +514,9 @@ def run_construct(args, cfg, rank, world, device, render=True):
         k0_s = stages["k0_pack_fft_sumsq_ms"] / 1e3
         res["k0_roofline"] = hbm_roofline("K0 pad + R2C + sum|b|^2 (FFT engine rows + columns)",
                                           m * H * W * C * 4 + m * C * Q * 8, k0_s,
-                                          "views read once (4 m H W C B) + spectra written once (8 m C Q B)")
+                                          "views read once (4 m H W C B) + spectra written once (8 m C Q B); "
+                                          "traffic: ncu DRAM bytes per construction (row pass + column pass)",
+                                          traffic=k1_traffic("k0_" + cfg))
     if V:
         res["render"] = {"value": V / t_ren_mean, "unit": "views/s", "ms": 1e3 * t_ren_mean,
                          "roofline": render_roofline(Q * n * (8 * C + 6), V // world if world > 1 else V,
