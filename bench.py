@@ -123,6 +123,21 @@ def k1_traffic(cfg: str):
         return None
 
 
+def parallelism_note(world: int) -> str:
+    return f"frequency-row slabs x{world} (chunked NCCL all-to-all), views x{world}" if world > 1 else "1 GPU"
+
+
+L2_NOTE = "inputs (views, spectra, layers) exceed the 126 MB L2; no explicit flush"
+
+
+def headline_config(m, H, W, C, n, pad, Q, c5_views, world) -> dict:
+    """The `config` of the headline workload: identical in both arms (ours / --impl reference)."""
+    return {"workload": f"c4+c5: c4: construct {m} views {H}x{W}x{C}, n={n} layers, pad {pad} (Q={Q} bins); then c5: "
+                        f"render {c5_views} views of a 64-layer 1920x1080x3 FDL (disk(1), f=2r)",
+            "bins": Q, "views": m, "layers": n, "channels": C, "render_views": c5_views,
+            "parallelism": parallelism_note(world), "l2": L2_NOTE}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -485,10 +500,8 @@ def run_construct(args, cfg, rank, world, device, render=True):
         "config": {"workload": f"{cfg}: construct {m} views {H}x{W}x{C}, n={n} layers, pad {pad} "
                                f"(Q={Q} bins)" + (f", then render {V} views" if V else ""),
                    "bins": Q, "views": m, "layers": n, "channels": C, "render_views": V,
-                   "parallelism": (f"frequency-row slabs x{world} (one NCCL all-to-all), views x{world}"
-                                   if world > 1 else "1 GPU"),
-                   "l2": "inputs (views, spectra, layers) exceed the 126 MB L2; no explicit flush",
-                   "k1_path": int(path)},
+                   "parallelism": parallelism_note(world), "l2": L2_NOTE},
+        "k1_path": int(path),
         "construct_ms": 1e3 * t_con_mean,
         "stages_ms": stages,
         "k1_ms": 1e3 * t_k1_mean,
@@ -744,9 +757,9 @@ def host_copy(t):
 def run_headline(args, rank, world, device):
     import torch
     res, case, dims = run_construct(args, "c4", rank, world, device, render=False)
-    res["config"]["workload"] = (f"c4+c5: {res['config']['workload']}; then c5: render {args.c5_views} views of a "
-                                 "64-layer 1920x1080x3 FDL (disk(1), f=2r) in "
-                                 f"{args.c5_batch}-view launches")
+    m_, n_, C_, H_, W_, pad_ = dims[:6]  # dims = (m, n, C, H, W, pad, Hp, Wp, Q, V)
+    res["config"] = headline_config(m_, H_, W_, C_, n_, pad_, dims[8], args.c5_views, world)
+    res["render_batch"] = args.c5_batch
     host_views = None
     c4s = None
     if world == 1:
@@ -763,7 +776,6 @@ def run_headline(args, rank, world, device):
     res["clocks"] = merge_clocks(clocks4, r5.pop("clocks"))
     res["gpu_launches"] += r5.pop("gpu_launches")
     res["render"] = r5
-    res["config"]["render_views"] = args.c5_views
     res["ms_per_step"] = res["construct_ms"] + r5["ms"]
     if world == 1 and not args.no_e2e:
         res["e2e"]["render"] = run_c5_e2e(args, model5, reqs5)
@@ -973,10 +985,7 @@ def run_reference_headline(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (harness/synth.py seeded occluded layered scene, SURVEY.md §8(d)); same seeds and "
                 "generator device as our arm",
-        "config": {"workload": f"c4+c5: c4: construct {m} views {H}x{W}x{C}, n={n} layers, pad {pad} (Q={Q} bins); "
-                               f"then c5: render {args.c5_views} views of a 64-layer 1920x1080x3 FDL "
-                               "(disk(1), f=2r)",
-                   "bins": Q, "views": m, "layers": n, "channels": C, "render_views": args.c5_views},
+        "config": headline_config(m, H, W, C, n, pad, Q, args.c5_views, args.gpus),
         "render": {"value": 1.0 / t5, "unit": "views/s", "s_per_view": t5},
         "construct_s_extrapolated": t4,
         "cpu_baseline": {"value": value, "unit": "freq·layers/s", "cores": max(cores4, cores5), "kind": "port",
