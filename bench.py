@@ -149,6 +149,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=64, help="render views per K3 launch (c1-c4 renders)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="also time the step as one CUDA-graph replay (paper_1901_06919_b200/graph.py); default on for c1")
     ap.add_argument("--cpu-sample-rows", type=int, default=None,
                     help="frequency rows solved per CPU sample step (default: 24, or 2 for c4)")
     ap.add_argument("--c5-views", type=int, default=C5_VIEWS, help="config 5: views rendered per step (all ranks)")
@@ -539,7 +541,33 @@ def run_construct(args, cfg, rank, world, device, render=True):
             res["render"]["k4_roofline"] = hbm_roofline(
                 "K4 inverse FFT + crop", V * (C * Q * 8 + H * W * C * 4), stages["k4_c2r_crop_ms"] / 1e3,
                 "spectra read once + images written once")
+    if (args.graph or cfg == "c1") and not sharded and not wide:
+        res["graph"] = run_graphed(args, case, reqs, Q, n)
     return res, case, (m, n, C, H, W, pad, Hp, Wp, Q, V)
+
+
+def run_graphed(args, case, reqs, Q, n):
+    """The same step (construction + renders) as ONE CUDA-graph replay for a fixed geometry."""
+    import importlib
+    import torch
+    import paper_1901_06919_b200 as fdl
+    G = importlib.import_module("paper_1901_06919_b200.graph")
+    views = fdl.ViewSet(images=case.views, u=case.u, v=case.v)
+    g = G.GraphedConstruct(views, fdl.ShiftParams.factored(case.u, case.v, case.d), requests=reqs)
+    for _ in range(max(args.warmup, 3)):
+        g()
+    g.check()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        g()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    return {"ms_per_step": ms, "value": Q * n / (ms / 1e3), "unit": "freq·layers per second of whole step",
+            "note": "construction + renders of the step as one CUDA-graph replay (views already in HBM; the host-driven "
+                    "fallbacks are replaced by a status check, GraphedConstruct.check)"}
 
 
 def run_construct_e2e(args, case, dims, device, host_views=None):

@@ -92,6 +92,20 @@ int fdl_selftest(double* max_err);
 int fdl_kernel_timer(int32_t enable);
 int fdl_kernel_timer_read(int32_t which, double* total_ms, int32_t* launches);
 
+/* CUDA-graph capture support.  The entry points stage their host parameter
+ * blocks through a reused pinned ring (a reuse waits on an event), which a
+ * captured graph must not depend on.  Between fdl_staging_arena_begin() and
+ * fdl_staging_arena_end() on this host thread every block is staged in a fresh
+ * pinned allocation owned by the arena and nothing synchronises, so the calls
+ * can be stream-captured (pass n_breakdown = NULL to fdl_solve_bins) and the
+ * graph replayed for as long as the arena lives; fdl_staging_arena_free()
+ * releases it after the graph is destroyed.  Warm every call up once before
+ * capturing (cuFFT plans, constant tables and kernel attributes are set up on
+ * first use). */
+void* fdl_staging_arena_begin(void);
+int fdl_staging_arena_end(void* arena);
+int fdl_staging_arena_free(void* arena);
+
 /* Test hook (not part of the reference interface): force_cufft = 1 makes K0 /
  * K4 on this host thread use cuFFT even where the library's own FFT engine
  * applies (grid sides 67 * 2^a, 131 * 2^a), so tests can compare the two. */

@@ -99,6 +99,9 @@ EXPORTS = {
     "fdl_kernel_timer": (ctypes.c_int, [ctypes.c_int32]),
     "fdl_kernel_timer_read": (ctypes.c_int, [ctypes.c_int32, c_double_p, c_int32_p]),
     "fdl_fft_force_cufft": (ctypes.c_int, [ctypes.c_int32]),
+    "fdl_staging_arena_begin": (ctypes.c_void_p, []),
+    "fdl_staging_arena_end": (ctypes.c_int, [ctypes.c_void_p]),
+    "fdl_staging_arena_free": (ctypes.c_int, [ctypes.c_void_p]),
     "fdl_default_lambda": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p,
                                           ctypes.c_void_p]),
     "fdl_views_to_spectra_workspace": (ctypes.c_size_t, [ctypes.c_int32] * 5),

@@ -132,8 +132,36 @@ struct StageRing {
 };
 thread_local std::map<int, StageRing> t_stage;
 
+// Graph-capture support (fdl_staging_arena_*): while an arena is open on this
+// thread, every parameter block goes to a fresh pinned allocation owned by the
+// arena -- never reused, no event recorded or waited on -- so the H2D copies a
+// CUDA graph captured meanwhile replays keep reading what was staged for them.
+// The K2 index scratch is allocated per call from the arena as well.
+struct StageArena {
+  std::vector<void*> pinned, device;
+};
+thread_local StageArena* t_arena = nullptr;
+
+// allocations are "potentially unsafe" calls under a global-mode stream capture
+struct RelaxedCapture {
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+  ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+};
+
 int upload(const Blob& b, void* dev, cudaStream_t st) {
   if (b.bytes.empty()) return FDL_OK;
+  if (t_arena) {
+    void* p = nullptr;
+    {
+      RelaxedCapture relaxed;
+      FDL_CUDA_CHECK(cudaMallocHost(&p, b.bytes.size()));
+    }
+    t_arena->pinned.push_back(p);
+    std::memcpy(p, b.bytes.data(), b.bytes.size());
+    FDL_CUDA_CHECK(cudaMemcpyAsync(dev, p, b.bytes.size(), cudaMemcpyHostToDevice, st));
+    return FDL_OK;
+  }
   int device = 0;
   FDL_CUDA_CHECK(cudaGetDevice(&device));
   StageRing& ring = t_stage[device];
@@ -167,6 +195,16 @@ struct IndexScratch {
 thread_local std::map<int, IndexScratch> t_index;
 
 int index_scratch(int count, cudaStream_t st, int** out) {
+  if (t_arena) {  // captured calls own their scratch
+    void* p = nullptr;
+    {
+      RelaxedCapture relaxed;
+      FDL_CUDA_CHECK(cudaMalloc(&p, sizeof(int) * std::max(count, 1)));
+    }
+    t_arena->device.push_back(p);
+    *out = reinterpret_cast<int*>(p);
+    return FDL_OK;
+  }
   int device = 0;
   FDL_CUDA_CHECK(cudaGetDevice(&device));
   IndexScratch& s = t_index[device];
@@ -186,6 +224,7 @@ int index_scratch(int count, cudaStream_t st, int** out) {
 }
 
 int index_scratch_done(cudaStream_t st) {
+  if (t_arena) return FDL_OK;
   int device = 0;
   FDL_CUDA_CHECK(cudaGetDevice(&device));
   IndexScratch& s = t_index[device];
@@ -797,6 +836,28 @@ using namespace fdl;
 extern "C" {
 
 int fdl_version(void) { return 100; }
+
+void* fdl_staging_arena_begin(void) {
+  if (t_arena) return nullptr;  // one open arena per thread
+  t_arena = new StageArena();
+  return t_arena;
+}
+
+int fdl_staging_arena_end(void* arena) {
+  if (!arena || arena != t_arena) return fail(FDL_ERR_INVALID, "fdl_staging_arena_end: not the open arena");
+  t_arena = nullptr;
+  return FDL_OK;
+}
+
+int fdl_staging_arena_free(void* arena) {
+  if (!arena) return FDL_OK;
+  if (arena == t_arena) t_arena = nullptr;
+  StageArena* a = reinterpret_cast<StageArena*>(arena);
+  for (void* p : a->pinned) cudaFreeHost(p);
+  for (void* p : a->device) cudaFree(p);
+  delete a;
+  return FDL_OK;
+}
 
 int fdl_kernel_timer(int32_t enable) {
   for (auto& v : t_ktimer.ev)
