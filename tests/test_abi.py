@@ -93,3 +93,31 @@ def test_calibration_entry_points_validate_without_gpu():
     assert lib.fdl_calib_workspace(ctypes.byref(d)) > 0
     assert lib.fdl_lstsq_minnorm_workspace(2, 3, 3, 1) > 0
     assert lib.fdl_lstsq_minnorm(-1, 3, 3, 1, None, None, None, None, None, 0, None) == nat.FDL_ERR_INVALID
+
+
+def test_on_device_decorator_passes_through_without_cuda_device():
+    """_native.on_device selects the CUDA device a call's tensors live on; host-only
+    calls (device None or a CPU device) run untouched."""
+    import torch
+    from paper_1901_06919_b200 import _native as nat
+
+    @nat.on_device(lambda x, device=None: device)
+    def probe(x, device=None):
+        return x + 1
+
+    assert probe(1) == 2
+    assert probe(1, device="cpu") == 2
+    assert probe(1, device=torch.device("cpu")) == 2
+    assert probe.__name__ == "probe"
+
+
+def test_staging_arena_lifecycle_without_gpu():
+    """The capture-support entry points are pure host bookkeeping until a call stages a block."""
+    from paper_1901_06919_b200 import _native as nat
+    L = nat.lib()
+    arena = L.fdl_staging_arena_begin()
+    assert arena
+    assert not L.fdl_staging_arena_begin()          # one open arena per thread
+    assert L.fdl_staging_arena_end(arena) == 0
+    assert L.fdl_staging_arena_end(arena) != 0      # already closed
+    assert L.fdl_staging_arena_free(arena) == 0
