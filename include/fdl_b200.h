@@ -12,6 +12,11 @@
  *   fdl_render_spectra     evaluate_scaled_grid + _weighted_layer_sum
  *                                                               lfmodel.py:101-122, render.py:190-207,238-245
  *   fdl_spectra_to_images  irfft_fast + crop + srgb_encode      spectra.py:202-208, render.py:210-225
+ *   fdl_audit_bins /       the 1e-8 normal-equation residual test and the minimum-norm
+ *   fdl_resolve_bins       fallback `_stacked_lstsq`                construct.py:157-165,196-210
+ *   fdl_calib_solve/_terms _solve_batch, _objective_terms, _grad_p  calibrate.py:139-229
+ *   fdl_view_sqerr         psnr / mse_per_channel numerators        pipeline.py:30-51
+ *   fdl_images_to_u8       the service's 8-bit quantisation         serve.py:127
  *
  * Conventions (all calls):
  *   - return 0 (FDL_OK) on success, a negative FDL_ERR_* code otherwise; the
