@@ -54,26 +54,58 @@ __host__ __device__ constexpr double c_angle(int e, int R) {  // 2 pi e / R fold
 __host__ __device__ constexpr float c_cos(int e, int R) { return (float)c_cos_series(c_angle(e, R)); }
 __host__ __device__ constexpr float c_sin(int e, int R) { return (float)c_sin_series(c_angle(e, R)); }
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 cmulf(float2 a, float2 w) {
-  return make_float2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
+// Complex values are packed (re, im) pairs in one 64-bit register (common.cuh: u64) and
+// every add / subtract / multiply is one packed fp32 instruction (FADD2 / FMUL2 / FFMA2):
+// half the issue slots of scalar code.  The swapped / negated forms of an operand are
+// SASS operand modifiers, not instructions.
+using cx = u64;
+__device__ __forceinline__ cx cadd(cx a, cx b) { return add2(a, b); }
+__device__ __forceinline__ cx csub(cx a, cx b) { return sub2(a, b); }
+__device__ __forceinline__ cx bcast(float s) { return pack2(s, s); }
+__device__ __forceinline__ cx mul2(cx a, cx b) {
+  cx r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// i * a = (-a.im, a.re); -i * a = (a.im, -a.re)
+__device__ __forceinline__ cx times_i(cx a) {
+  const float2 f = as_f2(a);
+  return pack2(-f.y, f.x);
+}
+__device__ __forceinline__ cx times_mi(cx a) {
+  const float2 f = as_f2(a);
+  return pack2(f.y, -f.x);
+}
+// a * (c + i s)
+__device__ __forceinline__ cx cmul_cs(cx a, float c, float s) {
+  cx r = mul2(a, bcast(c));
+  ffma2(r, times_i(a), bcast(s));
+  return r;
+}
+__device__ __forceinline__ cx cmulf(cx a, float2 w) { return cmul_cs(a, w.x, w.y); }
+// acc + a * s (s real)
+__device__ __forceinline__ cx fma_s(cx acc, cx a, float s) {
+  cx r = acc;
+  ffma2(r, a, bcast(s));
+  return r;
 }
 // x * (-i) forward / x * (+i) inverse
 template <bool INV>
-__device__ __forceinline__ float2 rot(float2 a) { return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x); }
+__device__ __forceinline__ cx rot(cx a) { return INV ? times_i(a) : times_mi(a); }
 
 // x * W_R^e, W_R = exp(-+ 2 pi i / R) (forward: minus), e and R compile-time
 template <int E, int R, bool INV>
-__device__ __forceinline__ float2 mul_root(float2 a) {
+__device__ __forceinline__ cx mul_root(cx a) {
   constexpr int e = ((E % R) + R) % R;
   if constexpr (e == 0) return a;
-  else if constexpr (2 * e == R) return make_float2(-a.x, -a.y);
-  else if constexpr (4 * e == R) return rot<INV>(a);
+  else if constexpr (2 * e == R) {
+    const float2 f = as_f2(a);
+    return pack2(-f.x, -f.y);
+  } else if constexpr (4 * e == R) return rot<INV>(a);
   else if constexpr (4 * e == 3 * R) return rot<!INV>(a);
   else {
     constexpr float c = c_cos(e, R), s = INV ? c_sin(e, R) : -c_sin(e, R);
-    return make_float2(a.x * c - a.y * s, a.x * s + a.y * c);
+    return cmul_cs(a, c, s);
   }
 }
 
@@ -83,8 +115,8 @@ struct Dft;
 
 template <bool INV>
 struct Dft<2, INV> {
-  __device__ static __forceinline__ void run(float2 (&v)[2]) {
-    const float2 a = v[0], b = v[1];
+  __device__ static __forceinline__ void run(cx (&v)[2]) {
+    const cx a = v[0], b = v[1];
     v[0] = cadd(a, b);
     v[1] = csub(a, b);
   }
@@ -92,12 +124,11 @@ struct Dft<2, INV> {
 
 template <bool INV>
 struct Dft<3, INV> {
-  __device__ static __forceinline__ void run(float2 (&v)[3]) {
-    const float2 t1 = cadd(v[1], v[2]);
-    const float2 t2 = make_float2(v[0].x - 0.5f * t1.x, v[0].y - 0.5f * t1.y);
-    const float2 d = csub(v[1], v[2]);
+  __device__ static __forceinline__ void run(cx (&v)[3]) {
+    const cx t1 = cadd(v[1], v[2]);
+    const cx t2 = fma_s(v[0], t1, -0.5f);
     constexpr float s = 0.86602540378443864676f;
-    const float2 r = rot<INV>(make_float2(s * d.x, s * d.y));  // -+ i s (b - c)
+    const cx r = rot<INV>(mul2(csub(v[1], v[2]), bcast(s)));  // -+ i s (b - c)
     v[0] = cadd(v[0], t1);
     v[1] = cadd(t2, r);
     v[2] = csub(t2, r);
@@ -106,9 +137,9 @@ struct Dft<3, INV> {
 
 template <bool INV>
 struct Dft<4, INV> {
-  __device__ static __forceinline__ void run(float2 (&v)[4]) {
-    const float2 a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
-    const float2 c = cadd(v[1], v[3]), d = rot<INV>(csub(v[1], v[3]));
+  __device__ static __forceinline__ void run(cx (&v)[4]) {
+    const cx a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
+    const cx c = cadd(v[1], v[3]), d = rot<INV>(csub(v[1], v[3]));
     v[0] = cadd(a, c);
     v[2] = csub(a, c);
     v[1] = cadd(b, d);
@@ -118,16 +149,16 @@ struct Dft<4, INV> {
 
 template <bool INV>
 struct Dft<5, INV> {
-  __device__ static __forceinline__ void run(float2 (&v)[5]) {
+  __device__ static __forceinline__ void run(cx (&v)[5]) {
     constexpr float c1 = 0.30901699437494742410f, c2 = -0.80901699437494742410f;
     constexpr float s1 = 0.95105651629515357212f, s2 = 0.58778525229247312917f;
-    const float2 t1 = cadd(v[1], v[4]), t2 = cadd(v[2], v[3]);
-    const float2 t3 = csub(v[1], v[4]), t4 = csub(v[2], v[3]);
-    const float2 a1 = make_float2(v[0].x + c1 * t1.x + c2 * t2.x, v[0].y + c1 * t1.y + c2 * t2.y);
-    const float2 a2 = make_float2(v[0].x + c2 * t1.x + c1 * t2.x, v[0].y + c2 * t1.y + c1 * t2.y);
-    const float2 b1 = rot<INV>(make_float2(s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y));  // -+ i (...)
-    const float2 b2 = rot<INV>(make_float2(s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y));
-    v[0] = make_float2(v[0].x + t1.x + t2.x, v[0].y + t1.y + t2.y);
+    const cx t1 = cadd(v[1], v[4]), t2 = cadd(v[2], v[3]);
+    const cx t3 = csub(v[1], v[4]), t4 = csub(v[2], v[3]);
+    const cx a1 = fma_s(fma_s(v[0], t1, c1), t2, c2);
+    const cx a2 = fma_s(fma_s(v[0], t1, c2), t2, c1);
+    const cx b1 = rot<INV>(fma_s(mul2(t3, bcast(s1)), t4, s2));   // -+ i (s1 t3 + s2 t4)
+    const cx b2 = rot<INV>(fma_s(mul2(t3, bcast(s2)), t4, -s1));  // -+ i (s2 t3 - s1 t4)
+    v[0] = cadd(cadd(v[0], t1), t2);
     v[1] = cadd(a1, b1);
     v[4] = csub(a1, b1);
     v[2] = cadd(a2, b2);
@@ -147,16 +178,16 @@ struct Dft {
   static_assert(A * B == R && B > 1, "radix must factor into 2, 3, 4, 5");
 
   template <int N2, int K1>
-  __device__ static __forceinline__ void twiddle_col(float2 (&s)[A]) {
+  __device__ static __forceinline__ void twiddle_col(cx (&s)[A]) {
     if constexpr (K1 < A) {
       s[K1] = mul_root<N2 * K1, R, INV>(s[K1]);
       twiddle_col<N2, K1 + 1>(s);
     }
   }
   template <int N2>
-  __device__ static __forceinline__ void first(const float2 (&v)[R], float2 (&t)[B][A]) {
+  __device__ static __forceinline__ void first(const cx (&v)[R], cx (&t)[B][A]) {
     if constexpr (N2 < B) {
-      float2 s[A];
+      cx s[A];
 #pragma unroll
       for (int n1 = 0; n1 < A; ++n1) s[n1] = v[n1 * B + N2];
       Dft<A, INV>::run(s);
@@ -166,12 +197,12 @@ struct Dft {
       first<N2 + 1>(v, t);
     }
   }
-  __device__ static __forceinline__ void run(float2 (&v)[R]) {
-    float2 t[B][A];
+  __device__ static __forceinline__ void run(cx (&v)[R]) {
+    cx t[B][A];
     first<0>(v, t);
 #pragma unroll
     for (int k1 = 0; k1 < A; ++k1) {
-      float2 s[B];
+      cx s[B];
 #pragma unroll
       for (int n2 = 0; n2 < B; ++n2) s[n2] = t[n2][k1];
       Dft<B, INV>::run(s);
@@ -254,16 +285,16 @@ __device__ __forceinline__ void pass(float2* buf, const float2* tw) {
       p = buf + b * PL::NP + blk * L + n2 + k0 * PL::PAD;
       stride = PASS == 0 ? M + PL::PAD : M;
     }
-    float2 v[R];
+    cx v[R];
 #pragma unroll
-    for (int n1 = 0; n1 < R; ++n1) v[n1] = p[n1 * stride];
+    for (int n1 = 0; n1 < R; ++n1) v[n1] = as_u64(p[n1 * stride]);
     Dft<R, INV>::run(v);
     if (M > 1) {
 #pragma unroll
       for (int k1 = 1; k1 < R; ++k1) v[k1] = cmulf(v[k1], twp[(k1 - 1) * M + n2]);
     }
 #pragma unroll
-    for (int k1 = 0; k1 < R; ++k1) p[k1 * stride] = v[k1];
+    for (int k1 = 0; k1 < R; ++k1) p[k1 * stride] = as_f2(v[k1]);
     if (LAYOUT == ROWS) {
       j += T;
       while (j >= PERVEC) {
