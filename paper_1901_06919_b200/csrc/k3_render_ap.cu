@@ -332,8 +332,9 @@ __global__ void __launch_bounds__(256, FDL_AP_MINB)
       double d0 = p.h_alpha[v] * ox + p.h_beta[v] * oy;
       t0 -= rint(t0);
       d0 -= rint(d0);
-      dl[b] = (float)d0;
-      th[b] = (float)t0 - dl[b];  // the loop adds the increment before use
+      // radians: x_k = th + k dl, |x_k| <= (2 n - 1) pi; one FFMA per (view, layer), no running sum
+      dl[b] = (float)(6.283185307179586476925 * d0);
+      th[b] = (float)(6.283185307179586476925 * t0);
     }
   }
 
@@ -367,6 +368,7 @@ __global__ void __launch_bounds__(256, FDL_AP_MINB)
 #pragma unroll
         for (int c = 0; c < C; ++c) Lnext[c] = inside ? ld_stream2(lp + c * Q) : make_float2(0.f, 0.f);
       }
+      const float kf = (float)(s * KLB + kl);
 #pragma unroll
       for (int b = 0; b < VB; ++b) {
         const float2 x = LXs[(b * KLB + kl) * TXA];
@@ -377,11 +379,11 @@ __global__ void __launch_bounds__(256, FDL_AP_MINB)
         ffma2(ab, hi2(T), pack2(y.x, y.x));        // (a, b) + fy (c, d)
         const float2 AB = as_f2(ab);
         const float sc = fmaf(x.x, AB.y, AB.x);    // psi
-        float t = th[b] + dl[b];
-        t -= rintf(t);                              // stay in [-1/2, 1/2]
-        th[b] = t;
+        // MUFU range-reduces the argument itself (x / 2 pi in fp32: <= 1.5e-5 rad at |x| = 200)
+        const float xk = fmaf(kf, dl[b], th[b]);
         float sn, cs;
-        __sincosf(6.283185307179586f * t, &sn, &cs);
+        asm("sin.approx.ftz.f32 %0, %1;" : "=f"(sn) : "f"(xk));
+        asm("cos.approx.ftz.f32 %0, %1;" : "=f"(cs) : "f"(xk));
         const u64 w = mul2s(pack2(cs, sn), sc);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
