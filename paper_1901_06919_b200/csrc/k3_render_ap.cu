@@ -204,13 +204,15 @@ __global__ void __launch_bounds__(256 * NG, NG == 1 ? 2 : 1)
 // is bound by the L1/shared data pipe (12 wavefronts per (view, bin, layer)
 // warp-instruction group: 16-byte column and row factors + the 16-byte quad).
 // Here the phase is generated instead of loaded:
-//   theta_vk(bin) = theta_v0(bin) + k delta_v(bin)   [turns, fp32, wrapped]
-//   w = (cos, sin)(2 pi theta)                        2 MUFU on the idle XU pipe
+//   x_vk(bin) = x_v0(bin) + k delta_v(bin)            [radians, one fp32 FFMA, no running sum]
+//   w = (cos, sin)(x)                                 2 MUFU on the idle XU pipe (sin/cos.approx.ftz)
 // so the factor entries shrink to the 8-byte lookup halves {frac, idx}: 2 + 1
-// shared wavefronts instead of 4 + 2.  theta_v0 and delta_v come from fp64
-// (pu_v0 wx + pv_v0 wy, alpha_v wx + beta_v wy, wrapped to [-1/2, 1/2]) once
-// per thread and view.  The self-conjugate Nyquist column / row, whose phases
-// are cosines (construct.py:68-80), are recomputed by render_ap_nyquist_fix.
+// shared wavefronts instead of 4 + 2.  x_v0 and delta_v come from fp64
+// (pu_v0 wx + pv_v0 wy, alpha_v wx + beta_v wy, wrapped to [-1/2, 1/2] turns, times
+// 2 pi) once per thread and view; |x_vk| <= (2 n - 1) pi, where the MUFU's own range
+// reduction is good to ~1.5e-5 rad (142 dB against the oracle at 1920 x 1080).
+// The self-conjugate Nyquist column / row, whose phases are cosines
+// (construct.py:68-80), are recomputed by render_ap_nyquist_fix.
 // ---------------------------------------------------------------------------
 constexpr int KLB = 8;  // layers per TMA stage of the 8-byte lookup entries
 
