@@ -63,7 +63,8 @@ __device__ inline Smem<PL> carve_and_build() {
 // warps of a CTA read the same interleaved image rows at about the same time.
 template <class PL>
 __global__ void __launch_bounds__(PL::THREADS, 1) fwd_rows_kernel(const float* __restrict__ views, int m, int H, int W,
-                                                                   int C, int pad, float2* __restrict__ t1, int srgb) {
+                                                                   int C, int pad, float2* __restrict__ t1, int srgb,
+                                                                   int gcs) {
   constexpr int N = PL::N, M = PL::M, T = PL::T, P = PL::P, Whp = N / 2 + 1;
   const Smem<PL> s = carve_and_build<PL>();
   const int lane = threadIdx.x % PL::TL;  // lane within the team
@@ -127,8 +128,13 @@ __global__ void __launch_bounds__(PL::THREADS, 1) fwd_rows_kernel(const float* _
       const int yp = rest % HP2, j = rest / HP2;
       const int y0 = 2 * yp;
       const bool has1 = y0 + 1 < H;
-      float2* o0 = t1 + (((size_t)j * C + c) * H + y0) * Whp;
-      float2* o1 = o0 + Whp;
+      // T1 is blocked for the column pass: [plane][column block of 2^gcs][row][2^gcs columns],
+      // so a column tile is ONE contiguous run of H * 2^gcs values (the scattered side of the
+      // transpose is this pass's stores, which nothing waits for, not the column pass's loads)
+      const int cblk = (Whp + (1 << gcs) - 1) >> gcs;
+      float2* o0 = t1 + ((size_t)(j * C + c) * cblk * H + y0) * (size_t)(1 << gcs);
+      const size_t bstep = (size_t)H << gcs;  // next column block, same row
+      const int gmask = (1 << gcs) - 1;
       const float2* b = s.buf + t * M;
       // k = k1 + P k2 and N - k = m1 + P m2, stepped incrementally (TL < P)
       int k1 = lane % P, k2 = lane / P;
@@ -137,8 +143,9 @@ __global__ void __launch_bounds__(PL::THREADS, 1) fwd_rows_kernel(const float* _
 #pragma unroll 2
       for (int k = lane; k < Whp; k += PL::TL) {
         const float2 z = b[k1 * PL::RS + k2], zc = b[m1 * PL::RS + m2];
-        o0[k] = make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y - zc.y));
-        if (has1) o1[k] = make_float2(0.5f * (z.y + zc.y), 0.5f * (zc.x - z.x));
+        float2* o = o0 + (size_t)(k >> gcs) * bstep + (k & gmask);
+        o[0] = make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y - zc.y));
+        if (has1) o[1 << gcs] = make_float2(0.5f * (z.y + zc.y), 0.5f * (zc.x - z.x));
         k1 += PL::TL;
         if (k1 >= P) {
           k1 -= P;
@@ -193,13 +200,14 @@ __global__ void __launch_bounds__(PL::THREADS, 1) fwd_cols_kernel(const float2* 
     const int kx = kx0 + gc;
     const bool colok = kx < Whp;
     {
-      const float2* src = t1 + (size_t)pl * H * Whp + kx;
+      // blocked T1 (see fwd_rows_kernel): the tile is contiguous, row stride GC
+      const float2* src = t1 + (size_t)item * H * GC + gc;
       constexpr int NI = (N + RG - 1) / RG;
       float2 v[NI];
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
         const int row = gr + i * RG - pad;
-        v[i] = (colok && (unsigned)row < (unsigned)H && gr + i * RG < N) ? __ldg(src + row * Whp)
+        v[i] = (colok && (unsigned)row < (unsigned)H && gr + i * RG < N) ? __ldg(src + row * GC)
                                                                           : make_float2(0.f, 0.f);
       }
 #pragma unroll
@@ -212,9 +220,8 @@ __global__ void __launch_bounds__(PL::THREADS, 1) fwd_cols_kernel(const float2* 
     {  // the next item's tile into L2 while this one transforms
       const int nx = item + gstride;
       if (nx < items) {
-        const int npl = nx / cblocks, nkx = (nx - npl * cblocks) * GC + gc;
-        const float2* src = t1 + (size_t)npl * H * Whp + min(nkx, Whp - 1);
-        for (int row = gr; row < H; row += 4 * RG) prefetch_l2(src + row * Whp);
+        const float2* src = t1 + (size_t)nx * H * GC;  // contiguous: one prefetch per 128 bytes
+        for (int e = gl * 16; e < H * GC; e += 16 * GL) prefetch_l2(src + e);
       }
     }
     fft2::transform<PL, false>(s.buf, s.tw2, lane);
@@ -536,9 +543,24 @@ bool fft_engine_applies(int Hp, int Wp, int C) {
   return !t_force_cufft && C >= 1 && C <= 4 && side_supported(Hp) && side_supported(Wp);
 }
 
+// column-group width of the column plan of side Hp (the block width of T1)
+int col_group(int Hp) {
+  int gc = 8;
+  with_plan(Hp, [&](auto pl) {
+    gc = decltype(pl)::GC;
+    return FDL_OK;
+  });
+  return gc;
+}
+
+size_t t1_elems(int m, int H, int W, int C, int pad) {
+  const int Hp = H + 2 * pad, Wp = W + 2 * pad, Whp = Wp / 2 + 1, gc = col_group(Hp);
+  return (size_t)m * C * ((Whp + gc - 1) / gc) * H * gc;
+}
+
 size_t engine_fwd_ws(int m, int H, int W, int C, int pad) {
   const int Wp = W + 2 * pad, Whp = Wp / 2 + 1;
-  return al256(sizeof(float2) * (size_t)m * C * H * Whp) + al256(sizeof(double) * (size_t)m * C * Whp);
+  return al256(sizeof(float2) * t1_elems(m, H, W, C, pad)) + al256(sizeof(double) * (size_t)m * C * Whp);
 }
 
 int engine_fwd(const float* views, int m, int H, int W, int C, int pad, float2* spectra, double* view_sumsq,
@@ -547,14 +569,17 @@ int engine_fwd(const float* views, int m, int H, int W, int C, int pad, float2* 
   const int Hp = H + 2 * pad, Wp = W + 2 * pad, Whp = Wp / 2 + 1;
   float2* t1 = reinterpret_cast<float2*>(ws);
   double* partial =
-      reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + al256(sizeof(float2) * (size_t)m * C * H * Whp));
+      reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + al256(sizeof(float2) * t1_elems(m, H, W, C, pad)));
+  const int gc = col_group(Hp);
+  int gcs = 0;
+  while ((1 << gcs) < gc) ++gcs;
   int rc = with_plan(Wp, [&](auto pl) {
     using PL = decltype(pl);
     auto k = fwd_rows_kernel<PL>;
     int r = prepare<PL>(k);
     if (r) return r;
     const int items = (m * ((H + 1) / 2) * C + PL::T - 1) / PL::T;
-    k<<<grid_for_items<PL>(items), PL::THREADS, PL::SMEM, st>>>(views, m, H, W, C, pad, t1, srgb);
+    k<<<grid_for_items<PL>(items), PL::THREADS, PL::SMEM, st>>>(views, m, H, W, C, pad, t1, srgb, gcs);
     FDL_LAUNCH_CHECK("fwd_rows_kernel");
     return FDL_OK;
   });
