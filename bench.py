@@ -333,8 +333,8 @@ def run_c5(args, rank, world, device):
                                        "traffic: ncu DRAM bytes per 256-view launch",
                                        traffic=k1_traffic("k4_c5") if batch == C5_BATCH else None),
            "clocks": clocks,
-           # per launch set: factor pre-pass + TMA aperture tile + K4 column pass + K4 row pass
-           "gpu_launches": args.steps * 4 * math.ceil(V / batch)}
+           # per launch set: lookup pre-pass + TMA aperture tile + Nyquist-line fix-up + K4 column pass + K4 row pass
+           "gpu_launches": args.steps * 5 * math.ceil(V / batch)}
     return res, model, reqs
 
 
