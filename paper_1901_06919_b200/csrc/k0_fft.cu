@@ -421,19 +421,31 @@ __global__ void __launch_bounds__(PL::THREADS, 1) inv_rows_kernel(const float2* 
       const int y0 = 2 * yp;
       const bool has1 = y0 + 1 < Ho;
       float* o0 = out + (((size_t)v * Ho + y0) * Wo) * C + c;
-      float* o1 = o0 + (size_t)Wo * C;
       const float2* b = s.buf + t * M;
+      // sample n = x + pad sits at slot (n % P) RS + n / P: stepped incrementally (TL < 2 P)
+      static_assert(PL::TL < 2 * PL::P, "at most two wraps per step");
+      int n1 = (lane + pad) % PL::P, n2 = (lane + pad) / PL::P;
+      const size_t ostep = (size_t)PL::TL * C;
+      float* p0 = o0 + (size_t)lane * C;
 #pragma unroll 4
-      for (int x = lane; x < Wo; x += PL::TL) {
-        const int n = x + pad;
-        const float2 z = b[PL::slot_out(n, 0)];
+      for (int x = lane; x < Wo; x += PL::TL, p0 += ostep) {
+        const float2 z = b[n1 * PL::RS + n2];
         float a0 = z.x * scale, a1 = z.y * scale;
         if (srgb) {
           a0 = srgb_enc_f(a0);
           a1 = srgb_enc_f(a1);
         }
-        o0[(size_t)x * C] = a0;
-        if (has1) o1[(size_t)x * C] = a1;
+        p0[0] = a0;
+        if (has1) p0[(size_t)Wo * C] = a1;
+        n1 += PL::TL;
+        if (n1 >= PL::P) {
+          n1 -= PL::P;
+          ++n2;
+        }
+        if (PL::TL > PL::P && n1 >= PL::P) {
+          n1 -= PL::P;
+          ++n2;
+        }
       }
     }
     fft2::team_sync<PL>();
