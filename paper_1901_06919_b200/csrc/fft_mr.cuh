@@ -229,6 +229,10 @@ struct Plan {
   __host__ __device__ static constexpr int phys(int pos) { return pos + (pos / M0) * PAD; }
   // where frequency (or, inverse, sample) k ends up
   __host__ __device__ static constexpr int where(int k) { return (k % R0) * M0 + ((k / R0) % R1) * M1 + k / (R0 * R1); }
+  // phys(where(k)) without the division by M0: the top-level block of where(k) is k % R0
+  __host__ __device__ static constexpr int phys_where(int k) {
+    return (k % R0) * (M0 + PAD) + ((k / R0) % R1) * M1 + k / (R0 * R1);
+  }
 };
 
 // the CTA's twiddle tables (every thread; caller syncs)

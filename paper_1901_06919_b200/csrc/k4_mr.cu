@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) mr_inv_rows_kernel(const float
       const float2* gb = buf + g * C * NP;
       for (int e = threadIdx.x; e < per_group; e += ROW_THREADS) {
         const int x = e / C, c = e - x * C;
-        const float2 z = gb[c * NP + PL::phys(PL::where(x + pad))];
+        const float2 z = gb[c * NP + PL::phys_where(x + pad)];
         float a0 = z.x * scale, a1 = z.y * scale;
         if (srgb) {
           a0 = srgb_enc_mr(a0);
