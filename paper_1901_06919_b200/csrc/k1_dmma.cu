@@ -22,6 +22,7 @@
 #include <algorithm>
 
 #include "k1_solve.cuh"
+#include "tma.cuh"
 
 namespace fdl {
 
@@ -39,6 +40,9 @@ constexpr int LD = 8;
 constexpr int kKUnroll = FDL_K1_KUNROLL;  // k-step loop unroll (A/B builds)
 #ifndef FDL_K1_TH
 #define FDL_K1_TH 1  // Toeplitz-Hankel Gram from spare RHS columns (0: Gram by DMMA, A/B)
+#endif
+#ifndef FDL_K1_TMA
+#define FDL_K1_TMA 1  // stage spectra / phase tables through the TMA unit where the layout allows
 #endif
 #ifndef FDL_K1_TH_PAIR_MINNB
 #define FDL_K1_TH_PAIR_MINNB 4
@@ -114,6 +118,11 @@ struct FastParams {
                         // 4 views x 2 layers of a quarter-warp hit distinct banks
   const double2* px_all;  // (Whp, nu, hwp) exp(2 pi i fl(u d_p) wx), cosine on the Nyquist column
   const double2* py_all;  // (nrows, nv, hwp); the shared-memory pitch, so staging is a flat copy
+  // TMA staging (mode 1, 16-byte plane stride): warps 2w and 2w + 1 solve the bins
+  // (kx, kx + 1) of one 16-byte word per plane; one tensor copy per `bs_box` planes
+  // lands the pair's spectra as a shared [plane][2] float2 tile, and each bin's
+  // phase-table column is one bulk copy
+  int tma, bs_box, bs_nbox;
 };
 
 __host__ __device__ constexpr int blk(int I, int J) { return I * (I + 1) / 2 + J; }
@@ -181,16 +190,18 @@ struct K1Cfg {
 };
 
 template <int NB, int MODE, int ODD, int PAIR>
-__global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, MODE, PAIR>::minb) k1_fast_kernel(SolveParams p, FastParams f) {
+__global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, MODE, PAIR>::minb) k1_fast_kernel(SolveParams p, FastParams f, const __grid_constant__ CUtensorMap smap) {
   constexpr int WARPS = K1Cfg<NB, MODE, PAIR>::warps;  // shadows the file-wide default
   constexpr int NBc = (NB - ODD) / 2;  // blocks of the cos half (= of the sin half), mode 1
   // blocks I, J interact (PAIR: only within a group)
   auto linked = [](int I, int J) { return !PAIR || grp(I, NBc) == grp(J, NBc); };
   constexpr int NBLK = NB * (NB + 1) / 2;
   constexpr int NP = NB * 8;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(128) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane >> 2, t = lane & 3;
   const int i = blockIdx.y;
+  const bool tma = MODE == MODE_SYMREAL && f.tma;
+  const int bss = tma ? 2 : 1;  // BS entries per (view, channel)
   const int ky = p.rows[i];
   const double oy = omega_y_label(ky, p.Hp);
   const bool nyq_y = (p.Hp % 2 == 0) && ky == p.Hp / 2;
@@ -209,7 +220,8 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
   // mode 1: per row (u-table offset, v-table offset, BS offset of j, of j' or -1)
   int4* ROW4 = reinterpret_cast<int4*>(PY + py_words);
   YEntry* YT = reinterpret_cast<YEntry*>(PY + py_words);
-  const int bs_words = (p.m * p.C + 1) & ~1;  // staged spectra, one float2 per (view, channel); keeps 16-B alignment
+  // staged spectra, one float2 per (view, channel); keeps 16-B alignment (TMA mode: own region below)
+  const int bs_words = tma ? 0 : ((p.m * p.C + 1) & ~1);
   constexpr int XW = xwords<NB, PAIR>();  // Toeplitz scratch (none when the Gram is formed by DMMA)
   const int per_warp = px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + XW + bs_words;
   // per column of the real system: (d^4 of its layer(s)) for the lam reg' diagonal
@@ -225,6 +237,22 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
   // W = L_KK^-1 of diagonal block K
   auto Wblk = [&](int K) { return K == NB - 1 ? S : Wst + K * 8 * LD; };
   float2* BS = reinterpret_cast<float2*>(X + XW);
+  // TMA mode: [2 mbarriers per warp | 128-byte aligned [plane][2] tile per warp pair] behind the
+  // per-warp regions; bar_px: this warp's phase-table column, bar_bs: the pair's spectra tile
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + rg_off + 2 * NP + WARPS * per_warp);
+  unsigned long long* bar_px = bars + 2 * warp;
+  unsigned long long* bar_bs = bars + 2 * (warp & ~1) + 1;
+  const bool lead = !(warp & 1);  // issues the pair's tensor copies
+  const unsigned bs_bytes = tma ? (unsigned)f.bs_nbox * f.bs_box * 16u : 0u;
+  if (tma) {
+    const unsigned off = (unsigned)(rg_off + 2 * NP + WARPS * per_warp + 2 * WARPS) * 8u;
+    BS = reinterpret_cast<float2*>(reinterpret_cast<char*>(smem) + ((off + 127u) & ~127u) + (warp >> 1) * bs_bytes);
+    if (lane == 0) {
+      mbar_init(bar_px, 1);
+      if (lead) mbar_init(bar_bs, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
 
   if (MODE == MODE_SYMREAL) {
     const double2* src = f.py_all + (size_t)i * f.nv * f.hwp;
@@ -233,7 +261,7 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
       int4 ro = make_int4(0, 0, 0, -1);
       if (e < mrow) {
         const int2 jj = PAIR ? p.row_pairs[e] : make_int2(e, -1);
-        ro = make_int4(f.u_idx[jj.x] * f.hwp, f.v_idx[jj.x] * f.hwp, jj.x * p.C, jj.y >= 0 ? jj.y * p.C : -1);
+        ro = make_int4(f.u_idx[jj.x] * f.hwp, f.v_idx[jj.x] * f.hwp, jj.x * p.C * bss, jj.y >= 0 ? jj.y * p.C * bss : -1);
       }
       ROW4[e] = ro;
     }
@@ -304,18 +332,71 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
     }
     cpa_commit();
   };
+  // TMA mode: a tensor copy must start on a 16-byte boundary, so the pairs are
+  // aligned on the flat bin index: rows at an odd offset shift their bins left by
+  // one (the first pair starts at kx = -1).  A warp whose bin lies outside the row
+  // while its partner's does not only takes part in the hand-over.
+  const int odd0 = tma ? (int)(sp_boff(p, i, 0) & 1) : 0;
+  auto kx_of = [&](int rep) { return (int)(blockIdx.x * p.reps + rep) * WARPS + warp - odd0; };
+  unsigned px_phase = 0, bs_phase = 0;
+  auto stage_px = [&](int kxs) {
+    if (lane == 0) {
+      const unsigned bytes = (unsigned)(f.nu * f.hwp) * 16u;
+      mbar_expect_tx(bar_px, bytes);
+      bulk_load(PX, f.px_all + (size_t)kxs * f.nu * f.hwp, bytes, bar_px);
+    }
+  };
+  auto stage_pair = [&](int kxp) {  // lead warp: the tile of bins (kxp, kxp + 1)
+    if (lane == 0) {
+      mbar_expect_tx(bar_bs, bs_bytes);
+      const int c0 = (int)(2 * (long long)sp_boff(p, i, 0)) + 2 * kxp;
+      for (int b = 0; b < f.bs_nbox; ++b) tma_load_2d(BS + 2 * b * f.bs_box, &smap, c0, b * f.bs_box, bar_bs);
+    }
+  };
+  // after a bin's k-steps: the pair hands the tile back (named barrier 1 + pair: the
+  // partner arrives, the lead waits and re-issues), each warp re-stages its own column
+  auto stage_next = [&](int rep) {
+    const int kxn = kx_of(rep + 1), kxpn = kxn - (warp & 1);
+    if (rep + 1 >= p.reps || kxpn >= p.Whp) return;  // pair-uniform
+    if (lead) {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");
+      stage_pair(kxpn);
+    } else {
+      asm volatile("bar.arrive %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");
+    }
+    if (kxn >= 0 && kxn < p.Whp) stage_px(kxn);
+  };
   {
-    const int kx0 = blockIdx.x * p.reps * WARPS + warp;
-    if (kx0 < p.Whp) stage_bin(kx0);
+    const int kx0 = kx_of(0);
+    if (tma) {
+      if (kx0 - (warp & 1) < p.Whp) {
+        if (lead) stage_pair(kx0);
+        if (kx0 >= 0 && kx0 < p.Whp) stage_px(kx0);
+      }
+    } else if (kx0 < p.Whp) {
+      stage_bin(kx0);
+    }
   }
   for (int rep = 0; rep < p.reps; ++rep) {
-  const int kx = (blockIdx.x * p.reps + rep) * WARPS + warp;
-  if (kx >= p.Whp) break;  // warp-uniform
-  const int kx_next = kx + WARPS;
+  const int kx = kx_of(rep);
+  if (kx - (tma ? (warp & 1) : 0) >= p.Whp) break;  // warp-uniform (TMA: pair-uniform)
+  if (tma && (kx < 0 || kx >= p.Whp)) {             // only the partner's bin exists
+    bs_phase ^= 1u;
+    stage_next(rep);
+    continue;
+  }
+  const int kx_next = kx_of(rep + 1);
   const bool has_next = rep + 1 < p.reps && kx_next < p.Whp;
   const double ox = omega_x_label(kx, p.Wp);
   const bool nyq_x = (p.Wp % 2 == 0) && kx == p.Wp / 2;
-  cpa_wait_all();
+  if (tma) {
+    mbar_wait(bar_px, px_phase);
+    px_phase ^= 1u;
+    mbar_wait(bar_bs, bs_phase);
+    bs_phase ^= 1u;
+  } else {
+    cpa_wait_all();
+  }
   __syncwarp();  // this bin's staged values visible to the whole warp
 
   double g[NBLK][2];
@@ -343,6 +424,7 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
   // two only, so no rounding beyond A's own).
   const bool bcol = q < 2 * p.C;
   const int bc = bcol ? (q >> 1) : 0;
+  const int bcs = bc * bss + (tma ? (warp & 1) : 0);  // BS index of this lane's channel (TMA: this bin of the pair)
   const double2* PX2 = reinterpret_cast<const double2*>(PX);
   const double2* PY2 = reinterpret_cast<const double2*>(PY);
 
@@ -358,11 +440,11 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
     bool paired = false;
     if (MODE == MODE_SYMREAL) {
       const int4 ro = ROW4[j];
-      const float2 b1 = BS[ro.z + bc];
+      const float2 b1 = BS[ro.z + bcs];
       const double v1 = bcol ? ((q & 1) ? (double)b1.y : (double)b1.x) : 0.0;
       if (PAIR) {
         paired = ro.w >= 0;
-        const float2 b2 = BS[paired ? ro.w + bc : bc];
+        const float2 b2 = BS[paired ? ro.w + bcs : bcs];
         const double v2 = (bcol && paired) ? ((q & 1) ? (double)b2.y : (double)b2.x) : 0.0;
         bf = v1 + v2;
         bfm = v1 - v2;
@@ -460,7 +542,8 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
   for (int r0 = 0; r0 < mfull; r0 += 4) kstep(r0, false);
   if (mfull < mrow) kstep(mfull, true);
   __syncwarp();  // every lane is done with BS / PX of this bin
-  if (has_next) stage_bin(kx_next);
+  if (tma) stage_next(rep);
+  else if (has_next) stage_bin(kx_next);
 
   if (MODE == MODE_SYMREAL && th) {
     // RHS columns 6/7 = M^T [Re A_0, Im A_0]  ->  t[r], r = 0..n-1  ->  G fragments
@@ -759,20 +842,56 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
 }
 
 template <int NB, int MODE, int ODD, int PAIR>
-int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
+int launch_fast(const SolveParams& p, const FastParams& f_in, cudaStream_t st) {
   constexpr int WARPS = K1Cfg<NB, MODE, PAIR>::warps;
+  FastParams f = f_in;
+  f.tma = 0;
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
   const int ro_words = (MODE == MODE_SYMREAL) ? 2 * ((p.mrow + 3) & ~3) : 3 * p.m * p.n;
-  const size_t smem = sizeof(double) * ((size_t)py_words + ro_words + 1 + 2 * NB * 8 +
-                                        (size_t)WARPS * (px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + xwords<NB, PAIR>() + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
-  if (smem > 220 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
+  const size_t fixed_words = (size_t)py_words + ro_words + 1 + 2 * NB * 8;
+  const size_t warp_words = px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + xwords<NB, PAIR>();
+  size_t smem = sizeof(double) * (fixed_words + (size_t)WARPS * (warp_words + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
+  // TMA staging of the spectra (FastParams::tma): needs 16-byte plane strides, bins in
+  // pairs, and room for the [plane][2] tiles
+  CUtensorMap smap{};
+  const size_t plane = (size_t)(p.plane_rows ? p.plane_rows : p.nrows) * p.Whp;
+  if (MODE == MODE_SYMREAL && FDL_K1_TMA && WARPS % 2 == 0 && plane % 2 == 0 && plane * 2 < (1ull << 31) &&
+      reinterpret_cast<uintptr_t>(p.spectra) % 16 == 0 && reinterpret_cast<uintptr_t>(f.px_all) % 16 == 0) {
+    const int planes = p.m * p.C;
+    // boxes of <= 256 planes, a multiple of 8 (128-byte shared-memory destinations); fewest padded planes
+    int nbox = 0, box = 0;
+    for (int nb = (planes + 255) / 256; nb <= (planes + 255) / 256 + 4; ++nb) {
+      const int bx = (((planes + nb - 1) / nb) + 7) & ~7;
+      if (bx <= 256 && (!nbox || nb * bx < nbox * box)) nbox = nb, box = bx;
+    }
+    const size_t tma_smem = ((sizeof(double) * (fixed_words + (size_t)WARPS * (warp_words + 2)) + 127) & ~(size_t)127) +
+                            (size_t)(WARPS / 2) * nbox * box * 16;
+    EncodeTiledFn enc = encode_tiled_fn();
+    if (enc && nbox && tma_smem <= 224 * 1024) {
+      const cuuint64_t gdim[2] = {(cuuint64_t)plane * 2, (cuuint64_t)planes};
+      const cuuint64_t gstride[1] = {(cuuint64_t)plane * 8};
+      const cuuint32_t bx[2] = {4, (cuuint32_t)box};
+      const cuuint32_t estr[2] = {1, 1};
+      const CUresult r = enc(&smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(p.spectra), gdim, gstride,
+                             bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r == CUDA_SUCCESS) {
+        f.tma = 1;
+        f.bs_box = box;
+        f.bs_nbox = nbox;
+        smem = tma_smem;
+      }
+    }
+  }
+  if (smem > 224 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
   auto kern = k1_fast_kernel<NB, MODE, ODD, PAIR>;
   FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (p.reps < 1) return fail(FDL_ERR_INVALID, "K1 fast path: reps < 1");
-  dim3 grid((unsigned)((p.Whp + WARPS * p.reps - 1) / (WARPS * p.reps)), (unsigned)p.nrows);
+  // (TMA pairs: rows at an odd flat offset are shifted left by one bin)
+  dim3 grid((unsigned)((p.Whp + f.tma + WARPS * p.reps - 1) / (WARPS * p.reps)), (unsigned)p.nrows);
   ktimer_mark(0, 0, st);
-  kern<<<grid, WARPS * 32, smem, st>>>(p, f);
+  kern<<<grid, WARPS * 32, smem, st>>>(p, f, smap);
   ktimer_mark(0, 1, st);
   FDL_LAUNCH_CHECK("k1_fast_kernel");
   return FDL_OK;
