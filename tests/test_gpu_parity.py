@@ -145,6 +145,32 @@ def test_asymmetric_view_set_matches_oracle(fdl):
     assert err <= max(LAYER_TOL, 10 * float(np.max(g["floor"])))
 
 
+@pytest.mark.parametrize("hw", [(24, 24), (23, 24), (24, 22), (23, 22), (21, 18), (24, 20)])
+def test_pair_staged_bins_match_oracle_on_odd_and_even_grids(fdl, hw):
+    # K1 stages the spectra of two neighbouring bins as one 16-byte word per plane (TMA tile per
+    # warp pair, aligned on the flat bin index): rows at odd offsets start a pair at kx = -1, rows
+    # of odd length end on a half pair, and an odd plane size falls back to per-lane copies
+    from oracle import fdl_oracle as O
+    g = load_golden("c2_s24")
+    H, W = hw
+    views = np.ascontiguousarray(g["views"][:, :H, :W])
+    sh = fdl.ShiftParams.factored(g["u"], g["v"], g["d"])
+    model = fdl.construct_fdl(fdl.ViewSet(images=views, u=g["u"], v=g["v"]), sh)
+    ref = O.construct(views, np.outer(g["u"], g["d"]), np.outer(g["v"], g["d"]), g["d"])
+    assert model.layers.shape == ref["layers"].shape
+    err = rel_l2(model.layers, ref["layers"])
+    print(f"{H}x{W}: grid {ref['hp']}x{ref['wp']} rel L2 {err:.3e}")
+    assert err <= max(LAYER_TOL, 10 * float(np.max(g["floor"])))
+    # G-weighted (well-determined directions only), so that a misplaced bin cannot hide behind the
+    # ill-conditioned low frequencies that dominate the plain norm
+    from gweight import g_weighted_error
+    args = (g["u"], g["v"], g["d"], ref["lam"], ref["hp"], ref["wp"])
+    gw = g_weighted_error(model.layers, ref["layers"], *args)
+    c64 = g_weighted_error(ref["layers"].astype(np.complex64), ref["layers"], *args)
+    print(f"  G-weighted {gw:.3e} (complex64 rounding of the oracle's layers {c64:.2e})")
+    assert gw <= max(GW_TOL, 3 * c64)
+
+
 @pytest.mark.parametrize("name", CASES)
 def test_render_matches_reference(fdl, name):
     g = load_golden(name)
