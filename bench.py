@@ -516,6 +516,11 @@ def run_construct(args, cfg, rank, world, device, render=True):
                      "traffic": k1_traffic(cfg) if world == 1 else None,
                      "algorithmic_bytes": 8 * C * (m + n) * q_k1,
                      "flops_per_bin": F_bin,
+                     # `achieved` counts the CANONICAL flops of the reference's complex solve;
+                     # the real re-writes execute roughly a quarter of them, so frac can exceed 1 while the
+                     # fp64 pipe is far from busy (ncu sm__pipe_fp64_cycles_active on C4, same kernel)
+                     "frac_counts": "canonical flops (the executed count is lower; see pipe_active_ncu)",
+                     "pipe_active_ncu": k1_traffic("k1_c4_fp64_pipe_active_ncu") if cfg in ("c4", "headline") else None,
                      "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r01_fp64_pipes.txt); "
                                     "MEASURED_PEAKS.json has no fp64 entry"},
         "clocks": clocks,
