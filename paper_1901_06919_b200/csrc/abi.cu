@@ -516,8 +516,7 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
     }
     // per-axis phase tables of the fast path: (Whp nu + nrows nv) hwp complex doubles,
     // hwp = the K1 shared-memory pitch of the n/2 + 1 entries (k1_dmma.cu)
-    const size_t hw = (size_t)(n / 2 + (n & 1));
-    const size_t hwp = hw + ((2 - hw % 8) + 8) % 8;
+    const size_t hwp = (size_t)k1_table_pitch(n);
     P.extra = 16 * hwp * ((size_t)p.Whp * p.fast_nu + (size_t)D->nrows * p.fast_nv);
   }
   return FDL_OK;

@@ -467,7 +467,8 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
 #pragma unroll
       for (int I = 0; I < NBc; ++I) {
         const int pp = I * 8 + q;
-        if (pp < h) {
+        // even n: table entries past h are zero-filled (k1_table_pitch), no bound check needed
+        if (!ODD || pp < h) {
           const double2 x = pxr[pp], y = pyr[pp];
           mf[I] = fma(x.x, y.x, -x.y * y.y);
           mf[I + NBc] = -fma(x.x, y.y, x.y * y.x);
@@ -976,7 +977,7 @@ int k1_fast_launch(const SolveParams& p, cudaStream_t st, bool* handled) {
     NB = 2 * f.H8 / 8 + (p.n & 1);
     f.hw = h + (p.n & 1);
     if (f.hw == 0) return FDL_OK;
-    f.hwp = f.hw + ((2 - f.hw % 8) + 8) % 8;
+    f.hwp = k1_table_pitch(p.n);
     // distinct u / v values (uploaded with the parameter block by the caller)
     if (!p.fast_u_idx || !p.fast_tables) return FDL_OK;
     f.u_idx = p.fast_u_idx;

@@ -77,6 +77,15 @@ struct SolveParams {
 // lambda of this solve: the device scalar when the caller computed it there
 __device__ __forceinline__ double solve_lam(const SolveParams& p) { return p.lam_dev ? __ldg(p.lam_dev) : p.lam; }
 
+// Row pitch (double2 entries) of the mode-1 per-axis phase tables: covers the n/2 (+1 for odd n)
+// entries AND every column of the 8-wide blocks (zero-filled, so the k-steps read them
+// unconditionally), and is 2 (mod 8) so that 4 views x 2 layers of a quarter-warp hit distinct banks.
+__host__ __device__ inline int k1_table_pitch(int n) {
+  const int hw = n / 2 + (n & 1), h8 = ((n / 2 + 7) / 8) * 8;
+  const int w = hw > h8 ? hw : h8;
+  return w + ((2 - w % 8) + 8) % 8;
+}
+
 // spectra / layers addressing: slab buffers or full-grid buffers (plane_rows)
 __device__ __forceinline__ size_t sp_plane(const SolveParams& p) {
   return (size_t)(p.plane_rows ? p.plane_rows : p.nrows) * p.Whp;
