@@ -486,12 +486,16 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
     } else {  // MODE_REALA: A_jk = psi_j(t_jk wx, t_jk wy) (all shifts are zero)
       const float2 bcur = BS[(valid ? j : 0) * p.C + bc];
       bf = (bcol && valid) ? ((q & 1) ? (double)bcur.y : (double)bcur.x) : 0.0;
+      if (uq) {
+        // shared real aperture (warp-uniform): every lane evaluates its entry unconditionally on a
+        // clamped table address and masks the result, so the NB lookups of a k-step carry no control
+        // dependence and their loads / fp64 chains overlap
 #pragma unroll
-      for (int I = 0; I < NB; ++I) {
-        const int k = I * 8 + q;
-        if (valid && k < p.n && uq) {
-          // shared real aperture: x half of the bilinear lookup + one quad read
-          const YEntry ye = YT[j * p.n + k];
+        for (int I = 0; I < NB; ++I) {
+          const int k = I * 8 + q;
+          const bool on = valid && k < p.n;
+          // x half of the bilinear lookup + one quad read
+          const YEntry ye = YT[on ? j * p.n + k : 0];
           const double pos = (__dmul_rn(ye.t, ox) - u_xi0) * u_inv;
           const bool okx = (pos >= 0.0) && (pos <= (double)(u_cols - 1));
           const int ix = okx ? min((int)pos, u_cols - 2) : 0;
@@ -499,8 +503,14 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
           const int qi = okx ? min(ye.iyoff + ix, u_zero) : u_zero;
           const double2 top = uq[2 * qi], bot = uq[2 * qi + 1];
           const double gy = 1.0 - ye.fy, gx = 1.0 - fx;
-          mf[I] = (top.x * gy) * gx + (top.y * gy) * fx + (bot.x * ye.fy) * gx + (bot.y * ye.fy) * fx;
-        } else if (valid && k < p.n) {
+          const double val = (top.x * gy) * gx + (top.y * gy) * fx + (bot.x * ye.fy) * gx + (bot.y * ye.fy) * fx;
+          mf[I] = on ? val : 0.0;
+        }
+      } else {
+#pragma unroll
+      for (int I = 0; I < NB; ++I) {
+        const int k = I * 8 + q;
+        if (valid && k < p.n) {
           const YEntry ye = YT[j * p.n + k];
           if (ye.ai < 0) {
             mf[I] = 1.0;
@@ -524,6 +534,7 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
             }
           }
         }
+      }
       }
     }
 #pragma unroll
