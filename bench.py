@@ -620,6 +620,29 @@ def run_construct_e2e(args, case, dims, device, host_views=None):
     if V:
         out["render"] = {"value": V / float(np.mean(tr)), "unit": "views/s", "ms": 1e3 * float(np.mean(tr)),
                          "d2h_bytes_per_step": V * H * W * C * 8}  # float64 images, like the reference
+    if big and not wide:
+        # the same construction from 8-bit host views (the loader's on-disk format, reference io.py:54-59),
+        # decoded on the device: a secondary figure, the headline e2e stays on float32 host views
+        q8 = torch.empty(tuple(host_views.shape), dtype=torch.uint8, pin_memory=True)
+        for j in range(m):
+            q8[j].copy_((host_views[j].clamp(0, 1) * 255).round().to(torch.uint8))
+        vq = fdl.ViewSet(images=fdl.QuantisedImages(q8), u=case.u, v=case.v, s=case.s)
+
+        def qstep():
+            t0 = time.perf_counter()
+            model = fdl.construct_fdl(vq, sh)
+            res = model.layers_host()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            del model, res
+            return dt
+
+        qstep()
+        tq = [qstep() for _ in range(steps)]
+        out["quantised_views"] = {"value": Q * n / float(np.mean(tq)), "unit": "freq·layers/s",
+                                  "construct_ms": 1e3 * float(np.mean(tq)), "h2d_bytes_per_step": int(q8.numel()),
+                                  "note": "uint8 host views (QuantisedImages), decoded by fdl_dequantise_views"}
+        del q8, vq
     return out
 
 

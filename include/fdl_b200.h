@@ -17,6 +17,7 @@
  *   fdl_calib_solve/_terms _solve_batch, _objective_terms, _grad_p  calibrate.py:139-229
  *   fdl_view_sqerr         psnr / mse_per_channel numerators        pipeline.py:30-51
  *   fdl_images_to_u8       the service's 8-bit quantisation         serve.py:127
+ *   fdl_dequantise_views   the loader's 8- / 16-bit decode           io.py:54-59
  *
  * Conventions (all calls):
  *   - return 0 (FDL_OK) on success, a negative FDL_ERR_* code otherwise; the
@@ -365,6 +366,13 @@ int fdl_view_sqerr(const float* images_dev, const void* ref_dev, int32_t ref_is_
 /* out_dev[i] = uint8(round_half_even(clip(images_dev[i], 0, 1) * 255)), evaluated
  * in float64 like the service's encoder input (serve.py:127). */
 int fdl_images_to_u8(const float* images_dev, int64_t count, uint8_t* out_dev, void* stream);
+
+/* out_dev[i] = float32(float64(q_dev[i]) / (2^bits - 1)), bits = 8 (uint8 samples) or 16
+ * (uint16): the reference loader's decode (io.py:54-59, arr.astype(float64) / 255.0 or
+ * / 65535.0) followed by the float32 cast of the upload, evaluated on the device so that
+ * quantised views cross PCIe as 1 or 2 bytes per sample.  Correctly rounded fp64 division,
+ * then round-to-nearest-even to float32: bit-identical to the host decode. */
+int fdl_dequantise_views(const void* q_dev, int32_t bits, int64_t count, float* out_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@ Out of scope: CLI, HTTP service, viewer.
 """
 
 from .spectra import DFT_CONVENTION, FrequencyGrid
-from .lfmodel import GAMMA, LINEAR, ApertureSpec, FdlModel, ShiftParams, ViewSet, expand_shifts
+from .lfmodel import GAMMA, LINEAR, ApertureSpec, FdlModel, QuantisedImages, ShiftParams, ViewSet, expand_shifts
 from .construct import (
     DEFAULT_EPS,
     SOLVE_CHUNK,
@@ -78,6 +78,7 @@ __all__ = [
     "ApertureSpec",
     "FdlModel",
     "ShiftParams",
+    "QuantisedImages",
     "ViewSet",
     "expand_shifts",
     "DEFAULT_EPS",

@@ -143,6 +143,8 @@ EXPORTS = {
     "fdl_view_sqerr": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int32] * 5 + [
         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "fdl_images_to_u8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "fdl_dequantise_views": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p,
+                                            ctypes.c_void_p]),
     "fdl_spectra_to_images_workspace": (ctypes.c_size_t, [ctypes.c_int32] * 4),
     "fdl_spectra_to_images": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int32] * 8 + [
         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),

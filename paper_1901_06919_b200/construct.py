@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 from . import _native as nat
-from .lfmodel import GAMMA, LINEAR, FdlModel, ShiftParams, ViewSet, _is_torch
+from .lfmodel import GAMMA, LINEAR, FdlModel, QuantisedImages, ShiftParams, ViewSet, _is_torch
 from .spectra import FrequencyGrid
 
 __all__ = [
@@ -409,9 +409,14 @@ def views_to_spectra_host(images, pad, device, chunk_bytes: int = UPLOAD_CHUNK_B
     through a two-slot pinned staging ring.  K0 is batch-independent bit for
     bit (tests/test_gpu_sharded.py), so the result equals the one-shot call."""
     import torch
-    src = images if _is_torch(images) else torch.from_numpy(np.ascontiguousarray(images, dtype=np.float32))
-    if src.dtype != torch.float32 or not src.is_contiguous():
-        src = src.to(torch.float32).contiguous()
+    quant = images if isinstance(images, QuantisedImages) else None
+    if quant is not None:
+        # 8- / 16-bit views cross PCIe quantised and are decoded on the device (fdl_dequantise_views)
+        src = quant.torch_host()
+    else:
+        src = images if _is_torch(images) else torch.from_numpy(np.ascontiguousarray(images, dtype=np.float32))
+        if src.dtype != torch.float32 or not src.is_contiguous():
+            src = src.to(torch.float32).contiguous()
     m, H, W, C = src.shape
     Hp, Wp = H + 2 * pad, W + 2 * pad
     per = max(1, min(m, chunk_bytes // max(1, H * W * C * 4)))
@@ -427,24 +432,30 @@ def views_to_spectra_host(images, pad, device, chunk_bytes: int = UPLOAD_CHUNK_B
     copy = nat.copy_stream(device)
     copy.wait_stream(compute)  # views_dev was allocated on the compute stream
     pinned = src.is_pinned()
-    ring = [] if pinned else [torch.empty((per, H, W, C), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    ring = [] if pinned else [torch.empty((per, H, W, C), dtype=src.dtype, pin_memory=True) for _ in range(2)]
     ring_ev = [None, None]
+    # quantised input lands in its own device buffer and is decoded into views_dev on the compute stream
+    land = torch.empty((m, H, W, C), dtype=src.dtype, device=device) if quant is not None else views_dev
     for i, j0 in enumerate(range(0, m, per)):
         j1 = min(m, j0 + per)
         with torch.cuda.stream(copy):
             if pinned:
-                views_dev[j0:j1].copy_(src[j0:j1], non_blocking=True)
+                land[j0:j1].copy_(src[j0:j1], non_blocking=True)
             else:
                 b = i % 2
                 if ring_ev[b] is not None:
                     ring_ev[b].synchronize()  # the slot's previous H2D has drained
                 ring[b][:j1 - j0].copy_(src[j0:j1])
-                views_dev[j0:j1].copy_(ring[b][:j1 - j0], non_blocking=True)
+                land[j0:j1].copy_(ring[b][:j1 - j0], non_blocking=True)
                 ring_ev[b] = torch.cuda.Event()
                 ring_ev[b].record(copy)
             ev = torch.cuda.Event()
             ev.record(copy)
         compute.wait_event(ev)
+        if quant is not None:
+            nat.check(L.fdl_dequantise_views(land[j0].data_ptr(), quant.bits, (j1 - j0) * H * W * C,
+                                             views_dev[j0].data_ptr(), nat.stream_handle(device)),
+                      "fdl_dequantise_views")
         k0 = L.fdl_views_to_spectra_srgb if srgb else L.fdl_views_to_spectra
         nat.check(k0(views_dev[j0].data_ptr(), j1 - j0, H, W, C, pad, spectra[j0].data_ptr(), sumsq[j0:].data_ptr(),
                      ws.data_ptr(), ws.numel(), nat.stream_handle(device)), "fdl_views_to_spectra")

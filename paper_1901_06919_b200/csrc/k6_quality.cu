@@ -11,6 +11,10 @@
 //                     (serve.py:127: (clip(img, 0, 1) * 255).round().astype(uint8),
 //                     numpy's round-half-even, evaluated in float64) so a
 //                     response leaves the device as 1 byte per sample.
+//   fdl_dequantise_views  the loader's decode (io.py:54-59: arr.astype(float64) / 255.0
+//                     or / 65535.0) on the device, so 8- / 16-bit views cross PCIe as
+//                     1 / 2 bytes per sample instead of 4; float32(float64(v) / max),
+//                     bit for bit what the host decode followed by the float32 upload gives.
 #include "common.cuh"
 
 namespace fdl {
@@ -89,6 +93,34 @@ __global__ void images_to_u8_kernel(const float* __restrict__ img, size_t count,
   }
 }
 
+// 8-bit: the 256 possible results are formed once per CTA (correctly rounded fp64
+// division, then RN to float32) and looked up; 16 samples per thread through 16-byte loads
+__global__ void __launch_bounds__(256) dequant8_kernel(const uint8_t* __restrict__ q, size_t count,
+                                                       float* __restrict__ out) {
+  __shared__ float lut[256];
+  lut[threadIdx.x] = __double2float_rn(__ddiv_rn((double)threadIdx.x, 255.0));
+  __syncthreads();
+  const bool aligned = reinterpret_cast<uintptr_t>(q) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  const size_t vec = aligned ? count / 16 : 0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < vec; e += stride) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(q) + e);
+    const unsigned ws[4] = {w.x, w.y, w.z, w.w};
+    float4* o = reinterpret_cast<float4*>(out) + 4 * e;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      o[k] = make_float4(lut[ws[k] & 255u], lut[(ws[k] >> 8) & 255u], lut[(ws[k] >> 16) & 255u], lut[ws[k] >> 24]);
+  }
+  for (size_t e = vec * 16 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += stride) out[e] = lut[q[e]];
+}
+
+__global__ void __launch_bounds__(256) dequant16_kernel(const uint16_t* __restrict__ q, size_t count,
+                                                        float* __restrict__ out) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += stride)
+    out[e] = __double2float_rn(__ddiv_rn((double)q[e], 65535.0));
+}
+
 }  // namespace
 }  // namespace fdl
 
@@ -124,6 +156,24 @@ int fdl_images_to_u8(const float* images_dev, int64_t count, uint8_t* out_dev, v
   const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
   images_to_u8_kernel<<<grid, 256, 0, as_stream(stream)>>>(images_dev, (size_t)count, out_dev);
   FDL_LAUNCH_CHECK("images_to_u8_kernel");
+  return FDL_OK;
+}
+
+int fdl_dequantise_views(const void* q_dev, int32_t bits, int64_t count, float* out_dev, void* stream) {
+  using namespace fdl;
+  if (bits != 8 && bits != 16) return fail(FDL_ERR_INVALID, "fdl_dequantise_views: bits must be 8 or 16");
+  if (count < 0) return fail(FDL_ERR_INVALID, "fdl_dequantise_views: negative count");
+  if (count == 0) return FDL_OK;
+  if (!q_dev || !out_dev) return fail(FDL_ERR_INVALID, "fdl_dequantise_views: null buffer");
+  const size_t per = bits == 8 ? 256 * 16 : 256;
+  const size_t blocks = ((size_t)count + per - 1) / per;
+  const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+  cudaStream_t st = as_stream(stream);
+  if (bits == 8)
+    dequant8_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint8_t*>(q_dev), (size_t)count, out_dev);
+  else
+    dequant16_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(q_dev), (size_t)count, out_dev);
+  FDL_LAUNCH_CHECK("dequant_kernel");
   return FDL_OK;
 }
 

@@ -121,3 +121,23 @@ def test_staging_arena_lifecycle_without_gpu():
     assert L.fdl_staging_arena_end(arena) == 0
     assert L.fdl_staging_arena_end(arena) != 0      # already closed
     assert L.fdl_staging_arena_free(arena) == 0
+
+
+def test_quantised_images_decode_like_the_reference_loader():
+    # io.py:54-59: uint8 -> / 255.0, uint16 -> / 65535.0 in float64; ViewSet keeps them quantised
+    from paper_1901_06919_b200 import QuantisedImages, ViewSet
+    rng = np.random.default_rng(2)
+    for dtype, maxv in ((np.uint8, 255.0), (np.uint16, 65535.0)):
+        q = rng.integers(0, int(maxv) + 1, (3, 5, 4, 2)).astype(dtype)
+        qi = QuantisedImages(q)
+        assert qi.shape == q.shape and qi.bits == 8 * np.dtype(dtype).itemsize
+        assert np.array_equal(np.asarray(qi), q.astype(np.float64) / maxv)
+        assert np.asarray(qi, dtype=np.float32).dtype == np.float32
+        vs = ViewSet(images=qi, u=np.zeros(3), v=np.zeros(3))
+        assert vs.images is qi and vs.num_views == 3 and (vs.height, vs.width, vs.channels) == (5, 4, 2)
+    gray = QuantisedImages(np.zeros((2, 4, 4), np.uint8))
+    assert gray.shape == (2, 4, 4, 1)
+    with pytest.raises(ValueError):
+        QuantisedImages(np.zeros((2, 4, 4, 1), np.float32))
+    with pytest.raises(ValueError):
+        QuantisedImages(np.zeros((4, 4), np.uint8))
