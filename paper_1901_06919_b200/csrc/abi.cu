@@ -464,19 +464,9 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
         idx[j] = f;
       }
     };
-    std::vector<double> uv, vv;
-    std::vector<int> ui, vi;
-    distinct(D->u, m, uv, ui);
-    distinct(D->v, m, vv, vi);
-    P.o_uidx = B.add(ui.data(), sizeof(int) * m);
-    P.o_vidx = B.add(vi.data(), sizeof(int) * m);
-    P.o_uval = B.add(uv.data(), sizeof(double) * uv.size());
-    P.o_vval = B.add(vv.data(), sizeof(double) * vv.size());
-    p.fast_nu = (int)uv.size();
-    p.fast_nv = (int)vv.size();
-    P.has_axes = true;
     // mirror pairs (k1_solve.cuh): every view paired with its (-u, -v) twin or at the origin
     p.mrow = m;
+    std::vector<int> rp;
     if (mode == MODE_SYMREAL && D->force_path != 5) {
       std::vector<int> partner(m, -2);
       bool all = true;
@@ -499,14 +489,19 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
         }
       }
       if (all) {
-        std::vector<int> rp;
+        // the representative of a pair (whose A_j row and table columns K1 uses) is the view with
+        // u > 0 (or u = 0, v > 0): the x tables then cover the non-negative u only (half the
+        // shared memory per warp; a swapped pair's equations are the same rows times -1 in the
+        // sin group, so the Gram matrix and the right-hand sides are bit-identical)
         for (int j = 0; j < m; ++j) {
           if (partner[j] == -1) {
             rp.push_back(j);
             rp.push_back(-1);
           } else if (partner[j] > j) {
-            rp.push_back(j);
-            rp.push_back(partner[j]);
+            const int k = partner[j];
+            const bool keep = D->u[j] > 0.0 || (D->u[j] == 0.0 && D->v[j] > 0.0);
+            rp.push_back(keep ? j : k);
+            rp.push_back(keep ? k : j);
           }
         }
         p.mrow = (int)rp.size() / 2;
@@ -514,6 +509,35 @@ int plan_solve(const fdl_solve_desc* D, SolvePlan& P, int* mode_out) {
         P.has_pairs = true;
       }
     }
+    // distinct u / v values of the views K1 generates rows for (all views, or the pairs' representatives)
+    std::vector<double> uv, vv, us, vs_;
+    std::vector<int> ui, vi;
+    if (P.has_pairs) {
+      std::vector<int> sub, si, sj;
+      for (size_t e = 0; e < rp.size(); e += 2) sub.push_back(rp[e]);
+      for (int j : sub) {
+        us.push_back(D->u[j]);
+        vs_.push_back(D->v[j]);
+      }
+      distinct(us.data(), (int)sub.size(), uv, si);
+      distinct(vs_.data(), (int)sub.size(), vv, sj);
+      ui.assign(m, 0);
+      vi.assign(m, 0);
+      for (size_t e = 0; e < sub.size(); ++e) {
+        ui[sub[e]] = si[e];
+        vi[sub[e]] = sj[e];
+      }
+    } else {
+      distinct(D->u, m, uv, ui);
+      distinct(D->v, m, vv, vi);
+    }
+    P.o_uidx = B.add(ui.data(), sizeof(int) * m);
+    P.o_vidx = B.add(vi.data(), sizeof(int) * m);
+    P.o_uval = B.add(uv.data(), sizeof(double) * uv.size());
+    P.o_vval = B.add(vv.data(), sizeof(double) * vv.size());
+    p.fast_nu = (int)uv.size();
+    p.fast_nv = (int)vv.size();
+    P.has_axes = true;
     // per-axis phase tables of the fast path: (Whp nu + nrows nv) hwp complex doubles,
     // hwp = the K1 shared-memory pitch of the n/2 + 1 entries (k1_dmma.cu)
     const size_t hwp = (size_t)k1_table_pitch(n);

@@ -44,6 +44,9 @@ constexpr int kKUnroll = FDL_K1_KUNROLL;  // k-step loop unroll (A/B builds)
 #ifndef FDL_K1_TMA
 #define FDL_K1_TMA 1  // stage spectra / phase tables through the TMA unit where the layout allows
 #endif
+#ifndef FDL_K1_W12
+#define FDL_K1_W12 1  // 12-warp CTAs for 7-8 block mirror-pair systems (K1Cfg)
+#endif
 #ifndef FDL_K1_TH_PAIR_MINNB
 #define FDL_K1_TH_PAIR_MINNB 4
 #endif
@@ -181,17 +184,20 @@ __global__ void k1_axis_tables_kernel(SolveParams p, FastParams f) {
 #ifndef FDL_K1_PAIR_MINB
 #define FDL_K1_PAIR_MINB 3
 #endif
-template <int NB, int MODE, int PAIR>
+// W12: 12-warp CTAs for the mirror-pair systems of 7-8 blocks (C4) when their shared memory fits (TMA
+// staging, phase tables of the non-negative u only, Toeplitz scratch aliased onto the table column):
+// three warps per scheduler instead of two at 168 registers (tools/k1_occ_probe.py: -10 %; 10 warps lose)
+template <int NB, int MODE, int PAIR, int W12 = 0>
 struct K1Cfg {
   static constexpr bool pair_small = PAIR && NB > 2 && NB <= FDL_K1_PAIR3;
   static constexpr int warps =
-      (MODE == MODE_REALA && NB >= 5 && NB <= 6) ? FDL_K1_REALA_WARPS : (pair_small ? FDL_K1_PAIR_WARPS : WARPS);
+      W12 ? 12 : ((MODE == MODE_REALA && NB >= 5 && NB <= 6) ? FDL_K1_REALA_WARPS : (pair_small ? FDL_K1_PAIR_WARPS : WARPS));
   static constexpr int minb = NB <= 2 ? 3 : (pair_small ? FDL_K1_PAIR_MINB : (NB <= 6 ? 2 : 1));
 };
 
-template <int NB, int MODE, int ODD, int PAIR>
-__global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, MODE, PAIR>::minb) k1_fast_kernel(SolveParams p, FastParams f, const __grid_constant__ CUtensorMap smap) {
-  constexpr int WARPS = K1Cfg<NB, MODE, PAIR>::warps;  // shadows the file-wide default
+template <int NB, int MODE, int ODD, int PAIR, int W12 = 0>
+__global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<NB, MODE, PAIR, W12>::minb) k1_fast_kernel(SolveParams p, FastParams f, const __grid_constant__ CUtensorMap smap) {
+  constexpr int WARPS = K1Cfg<NB, MODE, PAIR, W12>::warps;  // shadows the file-wide default
   constexpr int NBc = (NB - ODD) / 2;  // blocks of the cos half (= of the sin half), mode 1
   // blocks I, J interact (PAIR: only within a group)
   auto linked = [](int I, int J) { return !PAIR || grp(I, NBc) == grp(J, NBc); };
@@ -223,20 +229,24 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
   // staged spectra, one float2 per (view, channel); keeps 16-B alignment (TMA mode: own region below)
   const int bs_words = tma ? 0 : ((p.m * p.C + 1) & ~1);
   constexpr int XW = xwords<NB, PAIR>();  // Toeplitz scratch (none when the Gram is formed by DMMA)
-  const int per_warp = px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + XW + bs_words;
+  // TMA mode: the Toeplitz scratch X lives in the table column's region (the next column is
+  // fetched after the Toeplitz build instead of right after the k-steps)
+  const int pxr_words = tma ? (px_words > XW ? px_words : XW) : px_words;
+  const int xw_alloc = tma ? 0 : XW;
+  const int per_warp = pxr_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + xw_alloc + bs_words;
   // per column of the real system: (d^4 of its layer(s)) for the lam reg' diagonal
   const int rg_off = py_words + ((ro_words + 1) & ~1);  // 16-byte aligned
   double2* RG = reinterpret_cast<double2*>(smem + rg_off);
   double* base = smem + rg_off + 2 * NP + warp * per_warp;
   double* PX = base;
-  double* D0 = PX + px_words;  // diagonal-block scratch (LDD layout) of block Ka ...
+  double* D0 = PX + pxr_words;  // diagonal-block scratch (LDD layout) of block Ka ...
   double* D1 = D0 + DSZ;       // ... and of Kb
   double* S = D1 + DSZ;
   double* Wst = S + 8 * LD;
-  double* X = Wst + (NB - 1) * 8 * LD;
+  double* X = tma ? PX : Wst + (NB - 1) * 8 * LD;
   // W = L_KK^-1 of diagonal block K
   auto Wblk = [&](int K) { return K == NB - 1 ? S : Wst + K * 8 * LD; };
-  float2* BS = reinterpret_cast<float2*>(X + XW);
+  float2* BS = reinterpret_cast<float2*>(Wst + (NB - 1) * 8 * LD + xw_alloc);
   // TMA mode: [2 mbarriers per warp | 128-byte aligned [plane][2] tile per warp pair] behind the
   // per-warp regions; bar_px: this warp's phase-table column, bar_bs: the pair's spectra tile
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + rg_off + 2 * NP + WARPS * per_warp);
@@ -364,7 +374,11 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
     } else {
       asm volatile("bar.arrive %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");
     }
-    if (kxn >= 0 && kxn < p.Whp) stage_px(kxn);
+  };
+  // this warp's next table column (after the Toeplitz build when that used the column's region)
+  auto stage_px_next = [&](int rep) {
+    const int kxn = kx_of(rep + 1);
+    if (rep + 1 < p.reps && kxn - (warp & 1) < p.Whp && kxn >= 0 && kxn < p.Whp) stage_px(kxn);
   };
   {
     const int kx0 = kx_of(0);
@@ -383,6 +397,7 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
   if (tma && (kx < 0 || kx >= p.Whp)) {             // only the partner's bin exists
     bs_phase ^= 1u;
     stage_next(rep);
+    stage_px_next(rep);
     continue;
   }
   const int kx_next = kx_of(rep + 1);
@@ -554,8 +569,12 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
   for (int r0 = 0; r0 < mfull; r0 += 4) kstep(r0, false);
   if (mfull < mrow) kstep(mfull, true);
   __syncwarp();  // every lane is done with BS / PX of this bin
-  if (tma) stage_next(rep);
-  else if (has_next) stage_bin(kx_next);
+  if (tma) {
+    stage_next(rep);
+    if (!(MODE == MODE_SYMREAL && th && XW > 0)) stage_px_next(rep);
+  } else if (has_next) {
+    stage_bin(kx_next);
+  }
 
   if (MODE == MODE_SYMREAL && th) {
     // RHS columns 6/7 = M^T [Re A_0, Im A_0]  ->  t[r], r = 0..n-1  ->  G fragments
@@ -633,6 +652,7 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
           g[blk(I, J)][e] = v;
         }
     __syncwarp();
+    if (tma) stage_px_next(rep);  // X (= the table column's region in TMA mode) is free again
   }
 
   // ---------------------------------------------------------------- 2. + lam reg'
@@ -853,17 +873,20 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR>::warps * 32, K1Cfg<NB, M
   }  // bins of this warp
 }
 
-template <int NB, int MODE, int ODD, int PAIR>
-int launch_fast(const SolveParams& p, const FastParams& f_in, cudaStream_t st) {
-  constexpr int WARPS = K1Cfg<NB, MODE, PAIR>::warps;
+// W12: returns FDL_OK with *launched = false when the 12-warp configuration does not apply
+template <int NB, int MODE, int ODD, int PAIR, int W12>
+int launch_fast_cfg(const SolveParams& p, const FastParams& f_in, cudaStream_t st, bool* launched) {
+  constexpr int WARPS = K1Cfg<NB, MODE, PAIR, W12>::warps;
+  constexpr int XW = xwords<NB, PAIR>();
+  *launched = false;
   FastParams f = f_in;
   f.tma = 0;
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
   const int ro_words = (MODE == MODE_SYMREAL) ? 2 * ((p.mrow + 3) & ~3) : 3 * p.m * p.n;
   const size_t fixed_words = (size_t)py_words + ro_words + 1 + 2 * NB * 8;
-  const size_t warp_words = px_words + 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD + xwords<NB, PAIR>();
-  size_t smem = sizeof(double) * (fixed_words + (size_t)WARPS * (warp_words + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
+  const size_t scratch_words = 2 * DSZ + 8 * LD + (NB - 1) * 8 * LD;
+  size_t smem = sizeof(double) * (fixed_words + (size_t)WARPS * (px_words + scratch_words + XW + (((size_t)p.m * p.C + 1) & ~(size_t)1)));
   // TMA staging of the spectra (FastParams::tma): needs 16-byte plane strides, bins in
   // pairs, and room for the [plane][2] tiles
   CUtensorMap smap{};
@@ -877,7 +900,9 @@ int launch_fast(const SolveParams& p, const FastParams& f_in, cudaStream_t st) {
       const int bx = (((planes + nb - 1) / nb) + 7) & ~7;
       if (bx <= 256 && (!nbox || nb * bx < nbox * box)) nbox = nb, box = bx;
     }
-    const size_t tma_smem = ((sizeof(double) * (fixed_words + (size_t)WARPS * (warp_words + 2)) + 127) & ~(size_t)127) +
+    // (the Toeplitz scratch shares the table column's region in this mode)
+    const size_t warp_words = (size_t)(px_words > XW ? px_words : XW) + scratch_words + 2;
+    const size_t tma_smem = ((sizeof(double) * (fixed_words + (size_t)WARPS * warp_words) + 127) & ~(size_t)127) +
                             (size_t)(WARPS / 2) * nbox * box * 16;
     EncodeTiledFn enc = encode_tiled_fn();
     if (enc && nbox && tma_smem <= 224 * 1024) {
@@ -896,8 +921,9 @@ int launch_fast(const SolveParams& p, const FastParams& f_in, cudaStream_t st) {
       }
     }
   }
+  if (W12 && !f.tma) return FDL_OK;  // the 12-warp CTA only fits with the TMA layout: caller falls back
   if (smem > 224 * 1024) return fail(FDL_ERR_UNSUPPORTED, "K1 fast path: phase tables exceed shared memory");
-  auto kern = k1_fast_kernel<NB, MODE, ODD, PAIR>;
+  auto kern = k1_fast_kernel<NB, MODE, ODD, PAIR, W12>;
   FDL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (p.reps < 1) return fail(FDL_ERR_INVALID, "K1 fast path: reps < 1");
   // (TMA pairs: rows at an odd flat offset are shifted left by one bin)
@@ -906,7 +932,18 @@ int launch_fast(const SolveParams& p, const FastParams& f_in, cudaStream_t st) {
   kern<<<grid, WARPS * 32, smem, st>>>(p, f, smap);
   ktimer_mark(0, 1, st);
   FDL_LAUNCH_CHECK("k1_fast_kernel");
+  *launched = true;
   return FDL_OK;
+}
+
+template <int NB, int MODE, int ODD, int PAIR>
+int launch_fast(const SolveParams& p, const FastParams& f, cudaStream_t st) {
+  bool launched = false;
+  if constexpr (MODE == MODE_SYMREAL && PAIR && NB >= 7 && FDL_K1_W12) {
+    const int rc = launch_fast_cfg<NB, MODE, ODD, PAIR, 1>(p, f, st, &launched);
+    if (rc != FDL_OK || launched) return rc;
+  }
+  return launch_fast_cfg<NB, MODE, ODD, PAIR, 0>(p, f, st, &launched);
 }
 
 template <int MODE, int ODD, int PAIR>
