@@ -15,6 +15,8 @@
 //      substitution y_K = W r_K, r_I -= L_IK y_K (DMMA) run interleaved;
 //   4. backward substitution x_K = W^T (y_K - sum_{I>K} L_IK^T x_I) (DMMA);
 //   5. x mapped back to complex layer coefficients, written as complex64.
+// Staging: the bin's spectra words and phase-table column arrive by TMA (a tile per
+// warp pair, a bulk copy per warp) where the plane stride allows, else by cp.async.
 //
 // DMMA fragment layouts (m8n8k4, row.col, f64; lane l, q = l>>2, t = l&3):
 //   A (8x4): A[q][t]   B (4x8): B[t][q]   C (8x8): C[q][2t], C[q][2t+1]
@@ -216,6 +218,8 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<
   // [PX: nu*hwp complex | D 2*73 | S 64 | Wst (NB-1)*64 | X NP*8 | BS].  Lifetimes let
   // buffers double up: the W = L^-1 of the last diagonal block lives in S, and
   // the Toeplitz build keeps t[] in X's upper half and E in its lower half.
+  // TMA mode: per warp [PX (= X after the k-steps) | D | S | Wst], then the mbarriers
+  // (2 per warp) and one 128-byte aligned [plane][2] spectra tile per warp PAIR.
   double* PY = smem;
   const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
