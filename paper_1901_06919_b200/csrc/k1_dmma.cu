@@ -521,8 +521,10 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<
           const double fx = pos - (double)ix;
           const int qi = okx ? min(ye.iyoff + ix, u_zero) : u_zero;
           const double2 top = uq[2 * qi], bot = uq[2 * qi + 1];
-          const double gy = 1.0 - ye.fy, gx = 1.0 - fx;
-          const double val = (top.x * gy) * gx + (top.y * gy) * fx + (bot.x * ye.fy) * gx + (bot.y * ye.fy) * fx;
+          // bilinear weights as two lerps along y and one along x (6 fp64 operations instead of 10;
+          // within an ulp of the product form)
+          const double left = fma(ye.fy, bot.x - top.x, top.x), right = fma(ye.fy, bot.y - top.y, top.y);
+          const double val = fma(fx, right - left, left);
           mf[I] = on ? val : 0.0;
         }
       } else {
