@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<
   // TMA mode: per warp [PX (= X after the k-steps) | D | S | Wst], then the mbarriers
   // (2 per warp) and one 128-byte aligned [plane][2] spectra tile per warp PAIR.
   double* PY = smem;
-  const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
+  const int py_words = (MODE == MODE_SYMREAL) ? 2 * (f.nv + 1) * f.hwp : 0;  // + one all-zero row (padding rows)
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
   // mode 1 equation rows: one per view, or one per mirror pair (p.mrow)
   const int mrow = (MODE == MODE_SYMREAL) ? p.mrow : p.m;
@@ -271,8 +271,12 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<
   if (MODE == MODE_SYMREAL) {
     const double2* src = f.py_all + (size_t)i * f.nv * f.hwp;
     for (int e = threadIdx.x; e < f.nv * f.hwp; e += blockDim.x) reinterpret_cast<double2*>(PY)[e] = src[e];
+    // rows past mrow (the last k-step's padding) read an all-zero y table row: A = 0, so they add
+    // nothing to the Gram matrix or the right-hand sides and need no special k-step
+    for (int e = threadIdx.x; e < f.hwp; e += blockDim.x)
+      reinterpret_cast<double2*>(PY)[f.nv * f.hwp + e] = make_double2(0.0, 0.0);
     for (int e = threadIdx.x; e < m4; e += blockDim.x) {
-      int4 ro = make_int4(0, 0, 0, -1);
+      int4 ro = make_int4(0, f.nv * f.hwp, 0, -1);
       if (e < mrow) {
         const int2 jj = PAIR ? p.row_pairs[e] : make_int2(e, -1);
         ro = make_int4(f.u_idx[jj.x] * f.hwp, f.v_idx[jj.x] * f.hwp, jj.x * p.C * bss, jj.y >= 0 ? jj.y * p.C * bss : -1);
@@ -573,9 +577,14 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<
   const int mfull = mrow & ~3;
   // (the 80-register split kernels of 3-4 blocks, C2, run faster without unrolling: 0.90 -> 0.86 ms)
   constexpr int KU = K1Cfg<NB, MODE, PAIR, W12>::pair_small ? 1 : kKUnroll;
+  if (MODE == MODE_SYMREAL) {
 #pragma unroll KU
-  for (int r0 = 0; r0 < mfull; r0 += 4) kstep(r0, false);
-  if (mfull < mrow) kstep(mfull, true);
+    for (int r0 = 0; r0 < m4; r0 += 4) kstep(r0, false);
+  } else {
+#pragma unroll KU
+    for (int r0 = 0; r0 < mfull; r0 += 4) kstep(r0, false);
+    if (mfull < mrow) kstep(mfull, true);
+  }
   __syncwarp();  // every lane is done with BS / PX of this bin
   if (tma) {
     stage_next(rep);
@@ -889,7 +898,7 @@ int launch_fast_cfg(const SolveParams& p, const FastParams& f_in, cudaStream_t s
   *launched = false;
   FastParams f = f_in;
   f.tma = 0;
-  const int py_words = (MODE == MODE_SYMREAL) ? 2 * f.nv * f.hwp : 0;
+  const int py_words = (MODE == MODE_SYMREAL) ? 2 * (f.nv + 1) * f.hwp : 0;  // + one all-zero row (padding rows)
   const int px_words = (MODE == MODE_SYMREAL) ? 2 * f.nu * f.hwp : 0;
   const int ro_words = (MODE == MODE_SYMREAL) ? 2 * ((p.mrow + 3) & ~3) : 3 * p.m * p.n;
   const size_t fixed_words = (size_t)py_words + ro_words + 1 + 2 * NB * 8;
