@@ -451,6 +451,9 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<
   const double2* PX2 = reinterpret_cast<const double2*>(PX);
   const double2* PY2 = reinterpret_cast<const double2*>(PY);
 
+  // spare-column weights of a paired row: column 6 (Re A_j0) counts twice in the cos group and
+  // not at all in the sin group, column 7 (Im A_j0) the other way round
+  const double sp_c = (q == 6) ? 2.0 : 0.0, sp_s = (q == 6) ? 0.0 : 2.0;
   // one k-step: 4 rows (views) r0..r0+3, lane row j = r0 + t
   auto kstep = [&](int r0, bool tail) {
     const int j = r0 + t;
@@ -480,9 +483,11 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<
         const double2 x0 = pxr[0], y0 = pyr[0];
         const double re = fma(x0.x, y0.x, -x0.y * y0.y), im = fma(x0.x, y0.y, x0.y * y0.x);
         if (PAIR) {
-          // the partner's A_j'0 = conj(A_j0): column 6 (Re) sums, column 7 (Im) cancels
-          bf = (q == 6) ? (paired ? 2.0 * re : re) : (paired ? 0.0 : im);
-          bfm = (q == 6) ? (paired ? 0.0 : re) : (paired ? 2.0 * im : im);
+          // the partner's A_j'0 = conj(A_j0): column 6 (Re) sums, column 7 (Im) cancels; the
+          // weights of a paired row are per-lane constants (sp_c, sp_s), exact powers of two
+          const double val = (q == 6) ? re : im;
+          bf = val * (paired ? sp_c : 1.0);
+          bfm = val * (paired ? sp_s : 1.0);
         } else {
           bf = (q == 6) ? re : im;
         }
