@@ -448,6 +448,8 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<
   const bool bcol = q < 2 * p.C;
   const int bc = bcol ? (q >> 1) : 0;
   const int bcs = bc * bss + (tma ? (warp & 1) : 0);  // BS index of this lane's channel (TMA: this bin of the pair)
+  const float* BSq = reinterpret_cast<const float*>(BS) + (q & 1);
+  const float bmask = bcol ? 1.f : 0.f;
   const double2* PX2 = reinterpret_cast<const double2*>(PX);
   const double2* PY2 = reinterpret_cast<const double2*>(PY);
 
@@ -466,12 +468,13 @@ __global__ void __launch_bounds__(K1Cfg<NB, MODE, PAIR, W12>::warps * 32, K1Cfg<
     bool paired = false;
     if (MODE == MODE_SYMREAL) {
       const int4 ro = ROW4[j];
-      const float2 b1 = BS[ro.z + bcs];
-      const double v1 = bcol ? ((q & 1) ? (double)b1.y : (double)b1.x) : 0.0;
+      // this lane's RHS column is the real (q even) or imaginary (q odd) part of channel bc:
+      // one 4-byte read, masked by a per-lane 1.0f / 0.0f (columns past 2 C carry no data)
+      const double v1 = (double)(BSq[2 * (ro.z + bcs)] * bmask);
       if (PAIR) {
         paired = ro.w >= 0;
-        const float2 b2 = BS[paired ? ro.w + bcs : bcs];
-        const double v2 = (bcol && paired) ? ((q & 1) ? (double)b2.y : (double)b2.x) : 0.0;
+        const float f2 = BSq[2 * ((paired ? ro.w : ro.z) + bcs)];
+        const double v2 = (double)((paired ? f2 : 0.f) * bmask);
         bf = v1 + v2;
         bfm = v1 - v2;
       } else {
